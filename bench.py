@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""bench.py -- GPts/s of the stencil time-stepping + dmp halo-swap path on 1..8 B200.
+
+Workload (BASELINE.json config 5, weak scaling; at N=1 it is the 1-GPU heat run):
+  3D heat diffusion, space_order=4 (13-point star, radius 2), fp32, 1024^3 core points per
+  GPU, slab decomposition (N x 1 x 1, dmp.swap of 2-plane faces over NVLink), synthetic
+  initial condition = the reference's deterministic initValue (buffer.cpp:142-179).
+  A "step" is one time step of the whole job (every rank: halo swap + stencil apply).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL plumbing)
+
+Prints ONE JSON line on rank 0.  See DESIGN.md section "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+BYTES_PER_POINT = 8  # fp32 heat: read u_in once, write u_out once
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxs.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sms.sort()
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": max(maxs), "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def _ncu_traffic(workload):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    p = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(extent=256, timesteps=2):
+    """The reference's own CPU path (oracle/_ref: the reference core compiled from its sources),
+    the `halogen bench` recipe (tools/halogen.cpp:296-318): buildKernel -> f32 -> initialFields
+    -> steady_clock around runSerialStencil.  Single-threaded by design (the interpreter is)."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    from oracle import REF_PATH, Port, Ref
+    if os.path.exists(REF_PATH):
+        ref = Ref()
+        mod = ref.build("heat", 3, extent, 4, True)
+        bufs = ref.L.hr_initial_fields(mod)
+        secs = ref.L.hr_time_serial(mod, bufs, timesteps)
+        kind = "reference"
+    else:  # the C restatement, one thread
+        import paper_2404_02218_b200 as hg
+        port = Port()
+        prog = hg.build_kernel(hg.KernelSpec("heat", 3, extent, 4, "f32"))
+        arrays = port.initial_fields(prog)
+        t0 = time.perf_counter()
+        port.run(prog, arrays, timesteps, nthreads=1)
+        secs = time.perf_counter() - t0
+        kind = "port"
+    pts = extent ** 3
+    return {"value": pts * timesteps / secs / 1e9, "unit": "GPts/s", "cores": 1, "kind": kind,
+            "sample": f"heat3d so4 f32 {extent}^3 x {timesteps} timesteps, runSerialStencil, "
+                      f"1 thread (host nproc={os.cpu_count()})",
+            "seconds": secs}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    from oracle import REF_PATH, Port, Ref
+    ext = args.ref_extent
+    if os.path.exists(REF_PATH):
+        ref = Ref()
+        mod = ref.build("heat", 3, ext, 4, True)
+        bufs = ref.L.hr_initial_fields(mod)
+        step = lambda: ref.L.hr_time_serial(mod, bufs, 1)  # noqa: E731
+        kind = "reference"
+    else:
+        import paper_2404_02218_b200 as hg
+        port = Port()
+        prog = hg.build_kernel(hg.KernelSpec("heat", 3, ext, 4, "f32"))
+        arrays = port.initial_fields(prog)
+
+        def step():
+            t0 = time.perf_counter()
+            port.run(prog, arrays, 1, nthreads=1)
+            return time.perf_counter() - t0
+        kind = "port"
+    for _ in range(args.warmup):
+        step()
+    total = sum(step() for _ in range(args.steps))
+    pts = ext ** 3
+    val = pts * args.steps / total / 1e9
+    out = {"metric": "GPts/s (heat3d so4 fp32 time steps)", "value": val, "unit": "GPts/s",
+           "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference initValue)",
+           "config": {"workload": f"heat3d_so4 sample {ext}^3 per step (bounded sample of "
+                                  f"BASELINE config 5's 1024^3/GPU)", "timesteps_per_step": 1},
+           "cpu_baseline": {"value": val, "unit": "GPts/s", "cores": 1, "kind": kind,
+                            "sample": f"{ext}^3 heat3d so4, one runSerialStencil timestep per "
+                                      f"bench step (single-threaded interpreter)"},
+           "e2e": {"value": val, "unit": "GPts/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_02218_b200 as hg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    sh = C.c_void_p(stream.cuda_stream)
+
+    E = args.extent
+    grid = [world, 1, 1] if args.grid is None else [int(x) for x in args.grid.split("x")]
+    assert int(grid[0] * grid[1] * grid[2]) == world
+    gext = [E * grid[0], E * grid[1], E * grid[2]]  # weak scaling: E^3 per GPU
+    glob = hg.build_kernel(hg.KernelSpec("heat", 3, E, 4, "f32")).with_extents(gext)
+    local, dc = glob.decompose(grid)
+    plan = hg.Plan(local, local_rank)
+    coord = hg.coord_from_rank(rank, grid)
+    origin = [coord[d] * dc.core[d] for d in range(3)]
+    plan.init_fields(origin=origin, stream=sh)
+    dmp = None
+    if world > 1:
+        dmp = hg.Dmp(plan, dc, rank)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, dmp.export())
+        for r, b in enumerate(blobs):
+            if r != rank:
+                dmp.import_peer(r, b)
+        dist.barrier()
+
+    def steps(k):
+        if dmp is None:
+            plan.run(k, stream=sh)
+        else:
+            dmp.run(k, stream=sh)
+
+    core_local = local.core_points()
+    steps(args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = plan.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        steps(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = plan.launch_count() - l0
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(t.item())
+    value = core_local * world * args.steps / (ms_max / 1e3) / 1e9
+
+    # dominant kernel alone (the star stencil), events on its stream, for the roofline
+    kev0, kev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kk = max(5, min(args.steps, 50))
+    torch.cuda.synchronize()
+    kev0.record(stream)
+    plan.run(kk, stream=sh)
+    kev1.record(stream)
+    torch.cuda.synchronize()
+    k_ms = kev0.elapsed_time(kev1) / kk
+    peak, peak_src = _peaks()
+    achieved = BYTES_PER_POINT * core_local / (k_ms / 1e3) / 1e9
+    traffic = _ncu_traffic("heat3d_so4_1024")
+
+    # end to end through the public API with HOST buffers: upload -> T steps -> download
+    e2e = None
+    if not args.no_e2e:
+        T = args.e2e_timesteps
+        host = []
+        for i in range(local.nfields):
+            lo, hi = local.field_bounds(i)
+            host.append(torch.empty([u - l for l, u in zip(lo, hi)], dtype=torch.float32,
+                                    pin_memory=True))
+        for i in range(local.nfields):  # the synthetic inputs live on the host
+            plan.download(i, host[i].numpy(), stream=sh)
+        h2d = sum(h.numel() * 4 for h in host)
+        d2h = h2d
+
+        def e2e_call():
+            for i in range(local.nfields):
+                plan.upload(i, host[i].numpy(), stream=sh)
+            plan.reset_binding()
+            if dmp is not None:
+                dmp.invalidate()
+            steps(T)
+            perm, _ = plan.binding()
+            for i in range(local.nfields):
+                plan.download(perm[i], host[i].numpy(), stream=sh)
+
+        e2e_call()  # warm
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        n_calls = args.e2e_calls
+        t0 = time.perf_counter()
+        for _ in range(n_calls):
+            e2e_call()
+        torch.cuda.synchronize()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        secs = float(el.item())
+        e2e = {"value": core_local * world * T * n_calls / secs / 1e9, "unit": "GPts/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "step": f"one runSerialStencil-style call: upload fields from pinned host, "
+                       f"{T} time steps, download the final binding (per rank)",
+               "calls": n_calls}
+
+    if rank == 0:
+        clocks = clk.summary()
+        out = {
+            "metric": "GPts/s per step at 1/2/4/8 B200 (fraction of HBM roofline) vs host-CPU "
+                      "reference",
+            "value": value, "unit": "GPts/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference initValue hash, buffer.cpp:142-179)",
+            "config": {"workload": "heat3d_so4_weak (BASELINE config 5; N=1 is the 1-GPU case)",
+                       "kernel": plan.kernel_name, "core_per_gpu": [E, E, E],
+                       "global_core": gext, "grid": grid, "halo": 2,
+                       "l2": "inputs >> 126 MB L2 (2 x 4.6 GB fields per GPU), no flush needed",
+                       "transport": "NVLink P2P put (CUDA IPC) + system-scope flags"
+                       if world > 1 else "none"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": plan.kernel_name, "kernel_ms": k_ms,
+                         "algorithmic_bytes_per_launch": BYTES_PER_POINT * core_local,
+                         "peak_source": peak_src},
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline()
+        print(json.dumps(out), flush=True)
+    if dmp is not None:
+        dmp.close()
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--extent", type=int, default=1024)
+    ap.add_argument("--grid", default=None, help="process grid AxBxC (default N x 1 x 1)")
+    ap.add_argument("--e2e-timesteps", type=int, default=100)
+    ap.add_argument("--e2e-calls", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-extent", type=int, default=128)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

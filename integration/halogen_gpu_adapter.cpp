@@ -1,0 +1,195 @@
+// halogen_gpu_adapter.cpp -- the reference-side drop-in (what a halogen maintainer would add).
+//
+// Same signatures as the reference's executors, same argument meaning and error behaviour,
+// but the time loop runs on the B200 through the C-ABI of libhalogen_b200.so:
+//
+//   halogen::exec::gpu::runSerialStencil   ==  exec::runSerialStencil  (serial.hpp:29-31)
+//       caller-owned host Buffers, mutated in place, result = the final binding (a
+//       permutation of the inputs); failures throw ir::TrapError.
+//   halogen::exec::gpu::simulate           ==  exec::simulate          (simulator.hpp:76-82)
+//       decomposed (dmp-level) module; never throws, ok=false + error text instead.  Ranks are
+//       spread over the process's GPUs; each rank's local buffers come from the reference's
+//       own scatterRank and go back through its gatherRank, so geometry is the reference's.
+//
+// Built by `make -C oracle adapter` against the reference headers (it reads ir::Operation via
+// integration/ir_to_hg.hpp); see INTEGRATION.md.
+#include "hg/hg.h"
+#include "ir_to_hg.hpp"
+
+#include "../oracle/ref_handles.hpp"
+
+#include "halogen/exec/buffer.hpp"
+#include "halogen/exec/serial.hpp"
+#include "halogen/exec/simulator.hpp"
+#include "halogen/ir/diagnostics.hpp"
+
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace halogen::exec::gpu {
+
+namespace {
+
+struct PlanGuard {
+  hg_plan *p = nullptr;
+  ~PlanGuard() { hg_plan_destroy(p); }
+};
+
+void checkHg(int st, const char *what) {
+  if (st != HG_OK)
+    throw ir::TrapError("", std::string(what) + ": " + hg_last_error());
+}
+
+void checkField(const hg_program &p, int i, const Buffer &b) {
+  const int es = p.dtype == HG_F32 ? 4 : 8;
+  if (b.elemWidth() != es || b.rank() != p.rank)
+    throw ir::TrapError("", "field " + std::to_string(i) + " does not match the function");
+  for (int d = 0; d < p.rank; ++d)
+    if (b.lb[static_cast<std::size_t>(d)] != p.fields[i].lb[d] ||
+        b.shape[static_cast<std::size_t>(d)] != p.fields[i].ub[d] - p.fields[i].lb[d])
+      throw ir::TrapError("", "field " + std::to_string(i) + " bounds do not match the type");
+}
+
+} // namespace
+
+std::vector<std::shared_ptr<Buffer>> runSerialStencil(ir::Operation &module,
+                                                      std::vector<std::shared_ptr<Buffer>> fields,
+                                                      std::int64_t timesteps, int device = 0) {
+  hg_ir::Converted c;
+  try {
+    c = hg_ir::convert(module);
+  } catch (const std::exception &e) {
+    throw ir::TrapError("", e.what());
+  }
+  c.prog.ops = c.ops.data();
+  if (static_cast<int>(fields.size()) != c.prog.nfields)
+    throw ir::TrapError("", "field count does not match the function");
+  for (int i = 0; i < c.prog.nfields; ++i)
+    checkField(c.prog, i, *fields[static_cast<std::size_t>(i)]);
+  PlanGuard g;
+  checkHg(hg_plan_create(&c.prog, device, &g.p), "hg_plan_create");
+  for (int i = 0; i < c.prog.nfields; ++i) {
+    auto &b = *fields[static_cast<std::size_t>(i)];
+    checkHg(hg_plan_upload(g.p, i, b.data.data(), b.data.size(), nullptr), "upload");
+  }
+  checkHg(hg_plan_run(g.p, timesteps, nullptr), "hg_plan_run");
+  for (int i = 0; i < c.prog.nfields; ++i) {
+    auto &b = *fields[static_cast<std::size_t>(i)];
+    checkHg(hg_plan_download(g.p, i, b.data.data(), b.data.size(), nullptr), "download");
+  }
+  std::vector<int32_t> perm(static_cast<std::size_t>(c.prog.nfields));
+  checkHg(hg_plan_binding(g.p, perm.data(), nullptr), "hg_plan_binding");
+  std::vector<std::shared_ptr<Buffer>> out;
+  for (int32_t p : perm)
+    out.push_back(fields[static_cast<std::size_t>(p)]);
+  return out;
+}
+
+SimResult simulate(ir::Operation &module, const std::vector<std::shared_ptr<Buffer>> &globalInit,
+                   const SimOptions &opts) {
+  SimResult res;
+  try {
+    auto geom = geometryOf(module);
+    if (!geom.ok()) {
+      res.error = geom.diagText();
+      return res;
+    }
+    const DecompGeometry &G = *geom;
+    hg_ir::Converted c = hg_ir::convert(module);
+    c.prog.ops = c.ops.data();
+    if (!c.decomposed) {
+      res.error = "module is not decomposed";
+      return res;
+    }
+    const std::size_t nf = static_cast<std::size_t>(c.prog.nfields);
+    if (globalInit.size() != nf) {
+      res.error = "initial field count does not match the module";
+      return res;
+    }
+    const int64_t P = G.ranks();
+    int ndev = 0;
+    hg_device_count(&ndev);
+    if (ndev < 1) {
+      res.error = "no CUDA device";
+      return res;
+    }
+    std::vector<PlanGuard> plans(static_cast<std::size_t>(P));
+    std::vector<hg_dmp *> dmps(static_cast<std::size_t>(P), nullptr);
+    struct DmpGuard {
+      std::vector<hg_dmp *> &d;
+      ~DmpGuard() {
+        for (auto *x : d)
+          hg_dmp_destroy(x);
+      }
+    } dg{dmps};
+    std::vector<std::vector<std::shared_ptr<Buffer>>> locals;
+    for (int64_t r = 0; r < P; ++r) {
+      auto &pl = plans[static_cast<std::size_t>(r)];
+      checkHg(hg_plan_create(&c.prog, static_cast<int>(r % ndev), &pl.p), "hg_plan_create");
+      locals.push_back(scatterRank(G, globalInit, r)); // the reference's own scatter
+      for (std::size_t i = 0; i < nf; ++i) {
+        auto &b = *locals.back()[i];
+        checkHg(hg_plan_upload(pl.p, static_cast<int>(i), b.data.data(), b.data.size(), nullptr),
+                "upload");
+      }
+      checkHg(hg_dmp_create(pl.p, &c.decomp, r, &dmps[static_cast<std::size_t>(r)]),
+              "hg_dmp_create");
+    }
+    checkHg(hg_sim_connect(dmps.data(), static_cast<int>(P)), "hg_sim_connect");
+    checkHg(hg_sim_run(dmps.data(), static_cast<int>(P), opts.timesteps, nullptr), "hg_sim_run");
+    std::vector<int32_t> perm(nf);
+    checkHg(hg_plan_binding(plans[0].p, perm.data(), nullptr), "hg_plan_binding");
+    for (std::size_t i = 0; i < nf; ++i)
+      res.fields.push_back(globalInit[static_cast<std::size_t>(perm[i])]->clone());
+    for (int64_t r = 0; r < P; ++r) {
+      std::vector<std::shared_ptr<Buffer>> fin;
+      for (std::size_t i = 0; i < nf; ++i) {
+        auto b = locals[static_cast<std::size_t>(r)][static_cast<std::size_t>(perm[i])];
+        checkHg(hg_plan_download(plans[static_cast<std::size_t>(r)].p, perm[i], b->data.data(),
+                                 b->data.size(), nullptr),
+                "download");
+        fin.push_back(b);
+      }
+      gatherRank(G, r, fin, res.fields); // the reference's own gather
+    }
+    res.ok = true;
+  } catch (const std::exception &e) {
+    res.ok = false;
+    res.error = e.what();
+  }
+  return res;
+}
+
+} // namespace halogen::exec::gpu
+
+// C entry points for the parity tests (tests/test_adapter.py) -- handles from oracle/ref_capi.
+extern "C" {
+
+void *hga_run_serial(void *mod, void *bufs, long long timesteps, char *err, int cap) {
+  try {
+    auto out = halogen::exec::gpu::runSerialStencil(*static_cast<hg_ref::Mod *>(mod)->m,
+                                                    static_cast<hg_ref::Bufs *>(bufs)->v,
+                                                    timesteps);
+    return new hg_ref::Bufs{std::move(out)};
+  } catch (const std::exception &e) {
+    std::snprintf(err, static_cast<size_t>(cap), "%s", e.what());
+    return nullptr;
+  }
+}
+
+void *hga_simulate(void *mod, void *global_init, long long timesteps, char *err, int cap) {
+  halogen::exec::SimOptions o;
+  o.timesteps = timesteps;
+  auto r = halogen::exec::gpu::simulate(*static_cast<hg_ref::Mod *>(mod)->m,
+                                        static_cast<hg_ref::Bufs *>(global_init)->v, o);
+  if (!r.ok) {
+    std::snprintf(err, static_cast<size_t>(cap), "%s", r.error.c_str());
+    return nullptr;
+  }
+  return new hg_ref::Bufs{std::move(r.fields)};
+}
+
+} // extern "C"

@@ -1,0 +1,425 @@
+"""halogen-b200: B200-native stencil time stepping + dmp halo swap (arXiv 2404.02218 path).
+
+Python host glue over the C-ABI of ``lib/libhalogen_b200.so`` (include/hg/hg.h).  The names
+mirror the reference's C++ API in /root/reference/proj/core (exec::buildKernel,
+exec::initialFields, exec::runSerialStencil, exec::bindingAfter, ir::dmp::*, exec::simulate);
+the compute always runs in the sm_100a kernels -- there is no CPU fallback in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field as dc_field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as capi
+from ._capi import HgDecomp, HgExchange, HgLayout, HgOp, HgProgram, check, lib
+
+__all__ = [
+    "KernelSpec", "Program", "Buffer", "Plan", "Dmp", "build_kernel", "initial_fields",
+    "init_value", "fill_init", "fingerprint", "binding_after", "run_serial_stencil",
+    "rank_from_coord", "coord_from_rank", "neighbor_rank", "local_interval", "exchanges",
+    "simulate", "gpts_per_sec", "csv_header", "csv_row",
+]
+
+_I64 = C.c_int64
+_DT = {capi.HG_F32: np.float32, capi.HG_F64: np.float64}
+
+
+def _i64(v: Sequence[int]):
+    return (_I64 * max(len(v), 1))(*v)
+
+
+# ---- Buffer: the host field (exec::Buffer, buffer.hpp:25-57) --------------------------------
+@dataclass
+class Buffer:
+    """Row-major host storage with the logical lower bound of its field type."""
+    data: np.ndarray          # shape == alloc shape, halo included, C order
+    lb: List[int]
+
+    @staticmethod
+    def for_bounds(dtype, lb: Sequence[int], ub: Sequence[int]) -> "Buffer":
+        shape = [u - l for l, u in zip(lb, ub)]
+        return Buffer(np.zeros(shape, dtype=dtype), list(lb))
+
+    @property
+    def shape(self):
+        return list(self.data.shape)
+
+    def clone(self) -> "Buffer":
+        return Buffer(self.data.copy(), list(self.lb))
+
+    def fingerprint(self) -> int:
+        return fingerprint(self.data)
+
+
+# ---- host algorithms ----------------------------------------------------------------------
+def init_value(field_idx: int, coord: Sequence[int]) -> float:
+    return lib().hg_init_value(field_idx, len(coord), _i64(coord))
+
+
+def fingerprint(arr: np.ndarray) -> int:
+    a = np.ascontiguousarray(arr)
+    return int(lib().hg_fingerprint(a.ctypes.data_as(C.c_void_p), a.nbytes))
+
+
+def binding_after(groups: Sequence[Sequence[int]], num_args: int, steps: int) -> List[int]:
+    glen = (C.c_int32 * max(len(groups), 1))(*[len(g) for g in groups])
+    flat = [i for g in groups for i in g]
+    gg = (C.c_int32 * max(len(flat), 1))(*flat)
+    out = (C.c_int32 * max(num_args, 1))()
+    check(lib().hg_binding_after(len(groups), glen, gg, num_args, steps, out))
+    return list(out[:num_args])
+
+
+def gpts_per_sec(core_points: int, steps: int, seconds: float) -> float:
+    return lib().hg_gpts_per_sec(core_points, steps, seconds)
+
+
+def csv_header() -> str:
+    return "label,core_points,steps,seconds,gpts_per_s"  # throughput.cpp:25-27
+
+
+def csv_row(label: str, core_points: int, steps: int, seconds: float) -> str:
+    return (f"{label},{core_points},{steps},{seconds:.17g},"
+            f"{gpts_per_sec(core_points, steps, seconds):.17g}")
+
+
+def rank_from_coord(coord: Sequence[int], grid: Sequence[int]) -> int:
+    return lib().hg_rank_from_coord(len(grid), _i64(coord), _i64(grid))
+
+
+def coord_from_rank(rank: int, grid: Sequence[int]) -> List[int]:
+    out = (_I64 * 3)()
+    lib().hg_coord_from_rank(len(grid), rank, _i64(grid), out)
+    return list(out[:len(grid)])
+
+
+def neighbor_rank(rank: int, direction: Sequence[int], grid: Sequence[int]) -> int:
+    return lib().hg_neighbor_rank(len(grid), rank, _i64(direction), _i64(grid))
+
+
+def local_interval(extent: int, parts: int, part: int):
+    lb, ub = _I64(), _I64()
+    lib().hg_local_interval(extent, parts, part, C.byref(lb), C.byref(ub))
+    return lb.value, ub.value
+
+
+def exchanges(core, below, above, grid=None, coord=None):
+    n = len(core)
+    out = (HgExchange * 6)()
+    k = lib().hg_exchanges(n, _i64(core), _i64(below), _i64(above),
+                           _i64(grid) if grid is not None else None,
+                           _i64(coord) if coord is not None else None, out, 6)
+    res = []
+    for e in out[:k]:
+        res.append({"at": list(e.at[:n]), "size": list(e.size[:n]),
+                    "offset": list(e.offset[:n]), "to": list(e.to[:n])})
+    return res
+
+
+# ---- programs --------------------------------------------------------------------------------
+@dataclass
+class KernelSpec:
+    """exec::KernelSpec (kernels.hpp:32-37) plus the element type of the retyped module."""
+    kind: str = "heat"
+    rank: int = 2
+    extent: int = 64
+    order: int = 2
+    dtype: str = "f32"
+
+
+class Program:
+    """An hg_program plus the op storage it points into (the step function of a module)."""
+
+    def __init__(self, prog: HgProgram, ops):
+        self.prog = prog
+        self.ops = ops
+        self.prog.ops = C.cast(self.ops, C.POINTER(HgOp))
+
+    @staticmethod
+    def build(spec: KernelSpec) -> "Program":
+        ops = (HgOp * capi.HG_MAX_OPS)()
+        prog = HgProgram()
+        dt = capi.HG_F32 if spec.dtype == "f32" else capi.HG_F64
+        check(lib().hg_build_kernel_program(spec.kind.encode(), spec.rank, spec.extent,
+                                            spec.order, dt, C.byref(prog), ops, capi.HG_MAX_OPS))
+        return Program(prog, ops)
+
+    @property
+    def rank(self) -> int:
+        return self.prog.rank
+
+    @property
+    def nfields(self) -> int:
+        return self.prog.nfields
+
+    @property
+    def dtype(self):
+        return _DT[self.prog.dtype]
+
+    def field_bounds(self, i: int):
+        b = self.prog.fields[i]
+        return list(b.lb[:self.rank]), list(b.ub[:self.rank])
+
+    def groups(self) -> List[List[int]]:
+        out, at = [], 0
+        for g in range(self.prog.ngroups):
+            n = self.prog.group_len[g]
+            out.append(list(self.prog.groups[at:at + n]))
+            at += n
+        return out
+
+    def core_points(self) -> int:
+        s = self.prog.store[0]
+        n = 1
+        for d in range(self.rank):
+            n *= s.ub[d] - s.lb[d]
+        return n
+
+    def kernel_family(self) -> str:
+        buf = C.create_string_buffer(128)
+        check(lib().hg_program_match(C.byref(self.prog), buf, 128))
+        return buf.value.decode()
+
+    def decompose(self, grid: Sequence[int]):
+        """The decompose pass: returns (local program, HgDecomp)."""
+        local = HgProgram()
+        dc = HgDecomp()
+        check(lib().hg_decompose_program(C.byref(self.prog), len(grid), _i64(grid),
+                                         C.byref(local), C.byref(dc)))
+        return Program(local, self.ops), dc
+
+    def with_extents(self, extents: Sequence[int]) -> "Program":
+        """The same step program over a non-cubic domain [0, extents) (buildKernel is cubic,
+        kernels.cpp:155-158): store regions become [0, e) and every field keeps its halo."""
+        p = HgProgram()
+        C.pointer(p)[0] = self.prog
+        r = p.rank
+        for k in range(p.nresults):
+            for d in range(r):
+                p.store[k].lb[d] = 0
+                p.store[k].ub[d] = extents[d]
+        for i in range(p.nfields):
+            for d in range(r):
+                below = self.prog.store[0].lb[d] - self.prog.fields[i].lb[d]
+                above = self.prog.fields[i].ub[d] - self.prog.store[0].ub[d]
+                p.fields[i].lb[d] = -below
+                p.fields[i].ub[d] = extents[d] + above
+        return Program(p, self.ops)
+
+    def op_list(self):
+        return [self.ops[i] for i in range(self.prog.nops)]
+
+
+def build_kernel(spec: KernelSpec) -> Program:
+    return Program.build(spec)
+
+
+def fill_init(buf: Buffer, field_idx: int, origin: Optional[Sequence[int]] = None) -> None:
+    """exec::fillInit on the host (used for the reference-layout host buffers of tests)."""
+    r = buf.data.ndim
+    idx = np.indices(buf.data.shape).reshape(r, -1).T
+    flat = buf.data.reshape(-1)
+    org = list(origin) if origin is not None else [0] * r
+    for k, raw in enumerate(idx):
+        coord = [int(buf.lb[d] + raw[d] + org[d]) for d in range(r)]
+        flat[k] = init_value(field_idx, coord)
+
+
+def initial_fields(prog: Program) -> List[Buffer]:
+    """exec::initialFields computed on the GPU (bit-identical), returned as host Buffers."""
+    plan = Plan(prog)
+    plan.init_fields()
+    out = [Buffer(plan.download(i), prog.field_bounds(i)[0]) for i in range(prog.nfields)]
+    plan.close()
+    return out
+
+
+# ---- plans -------------------------------------------------------------------------------------
+class Plan:
+    """Device-resident fields + compiled step (hg_plan)."""
+
+    def __init__(self, prog: Program, device: int = 0):
+        self.program = prog
+        h = C.c_void_p()
+        check(lib().hg_plan_create(C.byref(prog.prog), device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            lib().hg_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def kernel_name(self) -> str:
+        buf = C.create_string_buffer(128)
+        check(lib().hg_plan_kernel_name(self.h, buf, 128))
+        return buf.value.decode()
+
+    def layout(self, b: int) -> HgLayout:
+        L = HgLayout()
+        check(lib().hg_plan_layout(self.h, b, C.byref(L)))
+        return L
+
+    def init_fields(self, origin: Optional[Sequence[int]] = None, stream=None):
+        check(lib().hg_plan_init_fields(self.h, _i64(origin) if origin is not None else None,
+                                        stream))
+
+    def upload(self, b: int, arr: np.ndarray, stream=None):
+        a = np.ascontiguousarray(arr, dtype=self.program.dtype)
+        check(lib().hg_plan_upload(self.h, b, a.ctypes.data_as(C.c_void_p), a.nbytes, stream))
+
+    def download(self, b: int, out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
+        lo, hi = self.program.field_bounds(b)
+        shape = [u - l for l, u in zip(lo, hi)]
+        if out is None:
+            out = np.empty(shape, dtype=self.program.dtype)
+        check(lib().hg_plan_download(self.h, b, out.ctypes.data_as(C.c_void_p), out.nbytes,
+                                     stream))
+        return out
+
+    def run(self, steps: int, stream=None):
+        check(lib().hg_plan_run(self.h, steps, stream))
+
+    def binding(self):
+        perm = (C.c_int32 * capi.HG_MAX_FIELDS)()
+        steps = _I64()
+        check(lib().hg_plan_binding(self.h, perm, C.byref(steps)))
+        return list(perm[:self.program.nfields]), steps.value
+
+    def reset_binding(self):
+        check(lib().hg_plan_reset_binding(self.h))
+
+    def launch_count(self) -> int:
+        return int(lib().hg_plan_launch_count(self.h))
+
+    def pack(self, b: int, at, size, dst_ptr: int, stream=None):
+        check(lib().hg_plan_pack(self.h, b, _i64(at), _i64(size), C.c_void_p(dst_ptr), stream))
+
+    def unpack(self, b: int, at, size, src_ptr: int, stream=None):
+        check(lib().hg_plan_unpack(self.h, b, _i64(at), _i64(size), C.c_void_p(src_ptr),
+                                   stream))
+
+
+def run_serial_stencil(prog: Program, fields: List[Buffer], timesteps: int,
+                       device: int = 0) -> List[Buffer]:
+    """exec::runSerialStencil (serial.cpp:57-88) on the GPU.
+
+    ``fields`` bind to the step arguments in order and are updated in place; the result is the
+    final binding (result i is the buffer bound to argument i after the last rotation)."""
+    if len(fields) != prog.nfields:
+        raise ValueError("field count does not match the function")
+    plan = Plan(prog, device)
+    try:
+        for i, f in enumerate(fields):
+            plan.upload(i, f.data)
+        plan.run(timesteps)
+        for i, f in enumerate(fields):
+            plan.download(i, f.data)
+        perm, _ = plan.binding()
+    finally:
+        plan.close()
+    return [fields[p] for p in perm]
+
+
+# ---- dmp -------------------------------------------------------------------------------------
+class Dmp:
+    """One rank's halo-swap endpoint (hg_dmp) over a local plan."""
+
+    def __init__(self, plan: Plan, decomp: HgDecomp, rank: int):
+        self.plan = plan
+        h = C.c_void_p()
+        check(lib().hg_dmp_create(plan.h, C.byref(decomp), rank, C.byref(h)))
+        self.h = h
+        self.rank = rank
+
+    def close(self):
+        if self.h:
+            lib().hg_dmp_destroy(self.h)
+            self.h = None
+
+    def export(self) -> bytes:
+        n = C.c_size_t()
+        check(lib().hg_dmp_ipc_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(lib().hg_dmp_ipc_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[:n.value]
+
+    def import_peer(self, peer_rank: int, blob: bytes):
+        b = C.create_string_buffer(blob, len(blob))
+        check(lib().hg_dmp_ipc_import(self.h, peer_rank, b, len(blob)))
+
+    def run(self, steps: int, stream=None):
+        check(lib().hg_dmp_run(self.h, steps, stream))
+
+    def bytes_exchanged(self) -> int:
+        return int(lib().hg_dmp_bytes_exchanged(self.h))
+
+    def invalidate(self):
+        """Host data was uploaded: every halo is stale."""
+        check(lib().hg_dmp_invalidate(self.h))
+
+
+def simulate(prog: Program, grid: Sequence[int], global_init: List[Buffer], timesteps: int,
+             devices: Optional[Sequence[int]] = None) -> List[Buffer]:
+    """exec::simulate (simulator.cpp:1066-1203): decompose, scatter, run every rank on the
+    GPU(s) of this process with device halo swaps, gather the cores.
+
+    Result i = global field bound to slot i at the end, gathered over a copy of the initial
+    global buffer of that slot's origin (so the global-boundary ring is the initial one)."""
+    local, dc = prog.decompose(grid)
+    nranks = int(np.prod(grid))
+    ndev = lib_device_count()
+    devs = list(devices) if devices is not None else [r % max(ndev, 1) for r in range(nranks)]
+    plans, dmps = [], []
+    try:
+        for r in range(nranks):
+            pl = Plan(local, devs[r])
+            coord = coord_from_rank(r, grid)
+            for f in range(prog.nfields):
+                g = global_init[f]
+                llo, lhi = local.field_bounds(f)
+                sl = tuple(slice(llo[d] + coord[d] * dc.core[d] - g.lb[d],
+                                 lhi[d] + coord[d] * dc.core[d] - g.lb[d])
+                           for d in range(prog.rank))
+                pl.upload(f, g.data[sl])           # scatterRank (simulator.cpp:995-1025)
+            plans.append(pl)
+            dmps.append(Dmp(pl, dc, r))
+        arr = (C.c_void_p * nranks)(*[d.h for d in dmps])
+        check(lib().hg_sim_connect(arr, nranks))
+        check(lib().hg_sim_run(arr, nranks, timesteps, None))
+        perm, _ = plans[0].binding()
+        out = [global_init[perm[i]].clone() for i in range(prog.nfields)]
+        for r in range(nranks):                 # gatherRank (simulator.cpp:1027-1060)
+            coord = coord_from_rank(r, grid)
+            for i in range(prog.nfields):
+                loc = plans[r].download(perm[i])
+                llo, _ = local.field_bounds(perm[i])
+                g = out[i]
+                src = tuple(slice(local.prog.store[0].lb[d] - llo[d],
+                                  local.prog.store[0].ub[d] - llo[d]) for d in range(prog.rank))
+                dst = tuple(slice(local.prog.store[0].lb[d] + coord[d] * dc.core[d] - g.lb[d],
+                                  local.prog.store[0].ub[d] + coord[d] * dc.core[d] - g.lb[d])
+                            for d in range(prog.rank))
+                g.data[dst] = loc[src]
+        return out
+    finally:
+        for d in dmps:
+            d.close()
+        for p in plans:
+            p.close()
+
+
+def lib_device_count() -> int:
+    n = C.c_int()
+    lib().hg_device_count(C.byref(n))
+    return n.value

@@ -1,0 +1,76 @@
+// hg_internal.hpp -- shared declarations of the halogen-b200 library (not installed).
+#ifndef HG_INTERNAL_HPP
+#define HG_INTERNAL_HPP
+
+#include "hg/hg.h"
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace hg {
+
+// ---- errors (thread-local last error, hg_last_error) ----------------------------------
+int setError(int status, const std::string &msg);
+
+// ---- program analysis (program.cpp) ----------------------------------------------------
+enum class Family { Generic = 0, Star = 1 };
+enum StarKind { kHeat = 0, kWave = 1, kCopy = 2 };
+
+// The star-Laplacian family the generator emits (kernels.cpp:110-135, 205-226):
+//   lap = c*W0; for d in 0..rank-1, k in taps: lap = lap + (u[+k e_d] + u[-k e_d]) * W[d][k]
+//   heat: out = c + lap*S        wave: out = (cur*K2 - prev) + lap*S        copy: out = c
+struct StarSpec {
+  int kind = kHeat;
+  int rank = 0;
+  int ntaps = 0;     // 1: {1}, 2: {1,2}, 3: {1,2,4}
+  int radius = 0;    // largest tap
+  uint64_t w0 = 0;   // raw constant bits
+  uint64_t w[3][3] = {};
+  uint64_t scale = 0, two = 0;
+  int cur_operand = 0, prev_operand = -1;
+};
+
+struct Analysis {
+  Family family = Family::Generic;
+  StarSpec star;
+  std::string name;            // kernel family name
+  int64_t dom_lb[3] = {0, 0, 0}, dom_ub[3] = {1, 1, 1}; // apply domain (hull of stores)
+  std::vector<int> src;        // rotationSources
+  int period = 1;              // lcm of group lengths
+};
+
+// Validates + classifies.  Returns HG_OK or an error status (message set).
+int analyze(const hg_program &p, Analysis &out);
+int validateProgram(const hg_program &p);
+
+// ---- device layout -----------------------------------------------------------------------
+struct Layout {
+  int rank = 0, es = 4;
+  int64_t shape[3] = {1, 1, 1}; // logical alloc shape (unused dims = 1)
+  int64_t lb[3] = {0, 0, 0};
+  int64_t pitch = 0, col0 = 0, rows = 1;
+  size_t bytes() const { return static_cast<size_t>(pitch * rows) * es; }
+  int64_t logicalCount() const {
+    int64_t n = 1;
+    for (int d = 0; d < rank; ++d) n *= shape[d];
+    return n;
+  }
+};
+Layout makeLayout(const hg_bounds &b, int rank, int es, int64_t core_lb_last);
+
+// ---- generic (bytecode) program for the generic kernel ---------------------------------
+struct GOp {       // compact, slot-allocated
+  int32_t code;    // hg_opcode
+  int16_t dst, a, b;
+  int16_t operand;
+  int32_t pad;
+  int64_t delta;   // ACCESS: flattened element offset in the operand layout
+  uint64_t bits;   // CONST
+};
+
+uint64_t fnv1a(const void *p, size_t n);
+
+} // namespace hg
+
+#endif

@@ -1,0 +1,910 @@
+// kernels.cu -- sm_100a kernels of the stencil time-stepping + halo-swap path.
+//
+// Bit-exactness contract: the reference evaluates every apply point as a fixed DAG of IEEE
+// round-to-nearest f32/f64 ops with no FMA contraction (-ffp-contract=off,
+// proj/CMakeLists.txt:8-10; interpreter.cpp:495-506).  All arithmetic here goes through
+// __fadd_rn/__fmul_rn/... (never contracted) and this file is also built with -fmad=false.
+// Loads, schedules and data movement are free; operand pairing and evaluation order are not.
+#include "kernels.hpp"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <utility>
+
+namespace hg {
+
+DevLayout devLayout(const Layout &L) {
+  DevLayout d{};
+  for (int i = 0; i < 3; ++i) {
+    d.shape[i] = L.shape[i];
+    d.lb[i] = L.lb[i];
+  }
+  d.pitch = L.pitch;
+  d.col0 = L.col0;
+  d.rank = L.rank;
+  d.es = L.es;
+  return d;
+}
+
+namespace {
+
+int cudaErr(cudaError_t e, const char *what) {
+  if (e == cudaSuccess)
+    return HG_OK;
+  return setError(HG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---- exact arithmetic -----------------------------------------------------------------------
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
+
+template <typename T> __host__ __device__ inline T fromBits(uint64_t b);
+template <> __host__ __device__ inline float fromBits<float>(uint64_t b) {
+  uint32_t u = static_cast<uint32_t>(b);
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+template <> __host__ __device__ inline double fromBits<double>(uint64_t b) {
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+}
+
+// ---- mbarrier / TMA PTX -------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smemAddr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbarInit(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smemAddr(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbarExpectTx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemAddr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbarArrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smemAddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbarWait(uint64_t *bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done)
+                 : "r"(smemAddr(bar)), "r"(parity)
+                 : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tmaLoad3d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                          int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+               "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smemAddr(dst)),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+               "r"(smemAddr(bar))
+               : "memory");
+}
+
+// Calls f(mb + U, integral_constant<U>) for U = 0, 1, ... while it returns true.
+template <typename F, int... Us>
+__device__ __forceinline__ void unrolled(F &f, int mb, std::integer_sequence<int, Us...>) {
+  (void)(f(mb + Us, std::integral_constant<int, Us>{}) && ...);
+}
+
+// 4 consecutive elements (16 B for f32, 2x16 B for f64) from 16-byte-aligned memory
+template <typename T> struct V4 { T v[4]; };
+__device__ __forceinline__ V4<float> ld4(const float *p) {
+  float4 t = *reinterpret_cast<const float4 *>(p);
+  return {{t.x, t.y, t.z, t.w}};
+}
+__device__ __forceinline__ V4<double> ld4(const double *p) {
+  double2 a = reinterpret_cast<const double2 *>(p)[0];
+  double2 b = reinterpret_cast<const double2 *>(p)[1];
+  return {{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ void st4(float *p, const V4<float> &v) {
+  *reinterpret_cast<float4 *>(p) = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
+}
+__device__ __forceinline__ void st4(double *p, const V4<double> &v) {
+  reinterpret_cast<double2 *>(p)[0] = make_double2(v.v[0], v.v[1]);
+  reinterpret_cast<double2 *>(p)[1] = make_double2(v.v[2], v.v[3]);
+}
+
+// ---- star family ------------------------------------------------------------------------
+//
+// One CTA owns a TX x TY tile of (x, y) columns and a chunk of z planes (dim 0).  A producer
+// warp streams the tile's planes, with a PADX-wide x rim and an R-row y rim, into an NS-deep
+// shared-memory ring by TMA (one cp.async.bulk.tensor per plane, mbarrier complete_tx).
+// Consumer threads own 4 consecutive x points each; the centre values of the 2R+1 planes
+// around the output plane live in registers (the z queue), x/y neighbours are read from the
+// staged plane with 16-byte LDS.  Output planes are stored straight to HBM (STG.128).
+template <int RANK> struct StarGeom;
+template <> struct StarGeom<3> {
+  static constexpr int TXT = 16, TYT = 16;
+};
+template <> struct StarGeom<2> {
+  static constexpr int TXT = 32, TYT = 1;
+};
+
+template <typename T> struct StarParams {
+  int64_t plane;   // elements between consecutive dim-0 planes
+  int64_t pitch;   // elements between rows of the last dim
+  int64_t col0;    // element column of raw index 0 of the last dim
+  int zs, ys, xs;  // raw start of the output region
+  int nz, ny, nx;  // output extents
+  int tiles_x, tiles_y, chunk, nchunks;
+  int boundary_last;
+  T *out;
+  T w0, wz[3], wy[3], wx[3], scale, two;
+};
+
+template <int NT> struct Taps;
+template <> struct Taps<1> {
+  static constexpr int R = 1;
+  __device__ static constexpr int k(int i) { return 1; }
+};
+template <> struct Taps<2> {
+  static constexpr int R = 2;
+  __device__ static constexpr int k(int i) { return i + 1; }
+};
+template <> struct Taps<3> {
+  static constexpr int R = 4;
+  __device__ static constexpr int k(int i) { return i == 0 ? 1 : (i == 1 ? 2 : 4); }
+};
+
+template <typename T, int RANK, int NT, int KIND> struct StarCfg {
+  static constexpr int R = Taps<NT>::R;
+  static constexpr int RY = RANK == 3 ? R : 0;
+  static constexpr int TXT = StarGeom<RANK>::TXT, TYT = StarGeom<RANK>::TYT;
+  static constexpr int TX = TXT * 4, TY = TYT;
+  static constexpr int PADX = 4;
+  static constexpr int CW = TX + 2 * PADX;
+  static constexpr int ROWS = TY + 2 * RY;
+  static constexpr int NCONS = TXT * TYT;
+  static constexpr int NWARPS_C = NCONS / 32;
+  static constexpr int NTHREADS = NCONS + 32;
+  // CTAs per SM the register budget must allow (f32 3D: 3 for r<=2, 2 for r=4)
+  static constexpr int MINB = RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? 3 : 2) : 1) : 4;
+  static constexpr int DEPTH = RANK == 3 ? 3 : 4;
+  static constexpr int NS = R + 1 + DEPTH;
+  static constexpr int Q = 2 * R + 1;
+  static constexpr int STAGE = ROWS * CW;   // elements
+  static constexpr int SSTRIDE = (STAGE + int(128 / sizeof(T)) - 1) / int(128 / sizeof(T)) * int(128 / sizeof(T));
+  static constexpr int PSTAGE = TY * TX;    // elements (wave prev)
+  static constexpr bool WAVE = KIND == kWave;
+  static constexpr size_t SMEM =
+      128 + sizeof(T) * (size_t(NS) * SSTRIDE + (WAVE ? size_t(NS) * PSTAGE : 0)) +
+      2 * NS * sizeof(uint64_t);
+};
+
+template <typename T, int RANK, int NT, int KIND>
+__global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND>::NTHREADS,
+                                  StarCfg<T, RANK, NT, KIND>::MINB)
+    starKernel(const __grid_constant__ CUtensorMap tmCur,
+               const __grid_constant__ CUtensorMap tmPrev, const StarParams<T> P) {
+  using C = StarCfg<T, RANK, NT, KIND>;
+  constexpr int R = C::R, RY = C::RY, NS = C::NS, Q = C::Q;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  T *stages = reinterpret_cast<T *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  T *pstages = stages + size_t(NS) * C::SSTRIDE;
+  uint64_t *full = reinterpret_cast<uint64_t *>(pstages + (C::WAVE ? size_t(NS) * C::PSTAGE : 0));
+  uint64_t *empty = full + NS;
+
+  // unit -> (tile, chunk); optionally the z-boundary chunks go last
+  const int ntiles = P.tiles_x * P.tiles_y;
+  const int unit = blockIdx.x;
+  const int tile = unit % ntiles;
+  int chunk = unit / ntiles;
+  if (P.boundary_last && P.nchunks > 2)
+    chunk = chunk < P.nchunks - 2 ? chunk + 1 : (chunk == P.nchunks - 2 ? 0 : P.nchunks - 1);
+  const int txi = tile % P.tiles_x, tyi = tile / P.tiles_x;
+  const int xb = txi * C::TX, yb = tyi * C::TY;
+  const int zb = chunk * P.chunk;
+  const int n = min(P.chunk, P.nz - zb);
+  const int tid = threadIdx.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbarInit(&full[s], 1);
+      mbarInit(&empty[s], C::NWARPS_C);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (n <= 0)
+    return;
+
+  if (tid >= C::NCONS) {
+    // ---------------- producer warp ----------------
+    if (tid == C::NCONS) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur))
+                   : "memory");
+      const int cx = int(P.col0) + P.xs + xb - C::PADX;
+      const int cy = RANK == 3 ? P.ys + yb - RY : 0;
+      const int z0 = P.zs + zb - R;
+      constexpr uint32_t curBytes = uint32_t(C::STAGE * sizeof(T));
+      constexpr uint32_t prevBytes = uint32_t(C::PSTAGE * sizeof(T));
+      for (int i = 0; i < n + 2 * R; ++i) {
+        const int s = i % NS;
+        if (i >= NS)
+          mbarWait(&empty[s], uint32_t((i / NS - 1) & 1));
+        const bool wantPrev = C::WAVE && i >= R && i < n + R;
+        mbarExpectTx(&full[s], curBytes + (wantPrev ? prevBytes : 0u));
+        tmaLoad3d(stages + size_t(s) * C::SSTRIDE, &tmCur, &full[s], cx, cy, z0 + i);
+        if (wantPrev)
+          tmaLoad3d(pstages + size_t(s) * C::PSTAGE, &tmPrev, &full[s], cx + C::PADX,
+                    RANK == 3 ? P.ys + yb : 0, z0 + i);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int tx = tid % C::TXT, ty = tid / C::TXT;
+  const int lane = tid & 31;
+  const int x0 = tx * 4;
+  const int rowOwn = (ty + RY) * C::CW;   // own row in a stage
+  T q[Q][4];
+
+  auto release = [&](int s) {
+    __syncwarp();
+    if (lane == 0)
+      mbarArrive(&empty[s]);
+  };
+
+  // prologue: planes 0 .. 2R-1 (z = zb-R .. zb+R-1): centres into the queue
+#pragma unroll
+  for (int i = 0; i < 2 * R; ++i) {
+    const int s = i % NS;
+    mbarWait(&full[s], uint32_t((i / NS) & 1));
+    V4<T> c = ld4(stages + size_t(s) * C::SSTRIDE + rowOwn + C::PADX + x0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      q[i][j] = c.v[j];
+    if (i < R)
+      release(s);
+  }
+
+  const bool yok = RANK == 2 || (yb + ty < P.ny);
+  T *outRow = P.out + (int64_t(P.zs + zb) * P.plane +
+                       (RANK == 3 ? int64_t(P.ys + yb + ty) * P.pitch : 0) + P.col0 + P.xs +
+                       xb + x0);
+  const int xrem = P.nx - (xb + x0);
+
+  int sN = (2 * R) % NS, phN = ((2 * R) / NS) & 1; // stage/parity of the plane arriving
+  int sC = R % NS;                                  // stage of the plane being computed
+
+  // One output plane; U is the position inside the Q-periodic register queue, a compile-time
+  // constant so every queue index below is a register name.  Returns false past the chunk end.
+  auto plane = [&](int m, auto uc) -> bool {
+    constexpr int U = decltype(uc)::value;
+    if (m >= n)
+      return false;
+    // arrival of plane z+R: its centres enter the queue
+    mbarWait(&full[sN], uint32_t(phN));
+    {
+      const V4<T> c = ld4(stages + size_t(sN) * C::SSTRIDE + rowOwn + C::PADX + x0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        q[(U + 2 * R) % Q][j] = c.v[j];
+    }
+    if (++sN == NS) {
+      sN = 0;
+      phN ^= 1;
+    }
+    // x / y neighbours of plane z from its stage
+    const T *st = stages + size_t(sC) * C::SSTRIDE;
+    const V4<T> L = ld4(st + rowOwn + x0);
+    const V4<T> Rr = ld4(st + rowOwn + 2 * C::PADX + x0);
+    V4<T> yp[NT], ym[NT];
+    if constexpr (RANK == 3) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        yp[t] = ld4(st + rowOwn + Taps<NT>::k(t) * C::CW + C::PADX + x0);
+        ym[t] = ld4(st + rowOwn - Taps<NT>::k(t) * C::CW + C::PADX + x0);
+      }
+    }
+    V4<T> pv;
+    if constexpr (C::WAVE)
+      pv = ld4(pstages + size_t(sC) * C::PSTAGE + ty * C::TX + x0);
+    release(sC);
+    if (++sC == NS)
+      sC = 0;
+
+    constexpr int cz = (U + R) % Q;
+    V4<T> o;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const T c = q[cz][j];
+      // lap = c*W0; then d = 0 (z), 1 (y), rank-1 (x), taps ascending: the generator's
+      // op order (kernels.cpp:110-135), one IEEE op at a time
+      T acc = mul_(c, P.w0);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int k = Taps<NT>::k(t);
+        acc = add_(acc, mul_(add_(q[(U + R + k) % Q][j], q[(U + R - k + Q) % Q][j]), P.wz[t]));
+      }
+      if constexpr (RANK == 3) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+          acc = add_(acc, mul_(add_(yp[t].v[j], ym[t].v[j]), P.wy[t]));
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int k = Taps<NT>::k(t);
+        const int ip = 4 + j + k, im = 4 + j - k; // window [L | centre | Rr]
+        const T xp = ip < 4 ? L.v[ip & 3] : (ip < 8 ? q[cz][ip & 3] : Rr.v[ip & 3]);
+        const T xm = im < 4 ? L.v[im & 3] : (im < 8 ? q[cz][im & 3] : Rr.v[im & 3]);
+        acc = add_(acc, mul_(add_(xp, xm), P.wx[t]));
+      }
+      if constexpr (C::WAVE)
+        o.v[j] = add_(sub_(mul_(c, P.two), pv.v[j]), mul_(acc, P.scale));
+      else
+        o.v[j] = add_(c, mul_(acc, P.scale));
+    }
+    if (yok) {
+      T *dst = outRow + int64_t(m) * P.plane;
+      if (xrem >= 4) {
+        st4(dst, o);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < xrem)
+            dst[j] = o.v[j];
+      }
+    }
+    return true;
+  };
+
+  for (int mb = 0; mb < n; mb += Q)
+    unrolled(plane, mb, std::make_integer_sequence<int, Q>{});
+}
+
+template <typename T, int RANK, int NT, int KIND>
+int launchStarT(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
+  using C = StarCfg<T, RANK, NT, KIND>;
+  auto kern = starKernel<T, RANK, NT, KIND>;
+  static std::once_flag once;
+  static cudaError_t attrErr = cudaSuccess;
+  std::call_once(once, [&] {
+    attrErr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(C::SMEM));
+  });
+  if (attrErr != cudaSuccess)
+    return cudaErr(attrErr, "cudaFuncSetAttribute(star)");
+  const StarSpec &s = *L.spec;
+  StarParams<T> P{};
+  int zd = 0, yd = RANK == 3 ? 1 : -1, xd = RANK - 1;
+  P.pitch = L.lay.pitch;
+  P.plane = RANK == 3 ? L.lay.pitch * L.lay.shape[1] : L.lay.pitch;
+  P.col0 = L.lay.col0;
+  P.zs = int(L.start[zd]);
+  P.ys = RANK == 3 ? int(L.start[yd]) : 0;
+  P.xs = int(L.start[xd]);
+  P.nz = int(L.ext[zd]);
+  P.ny = RANK == 3 ? int(L.ext[yd]) : 1;
+  P.nx = int(L.ext[xd]);
+  P.tiles_x = (P.nx + C::TX - 1) / C::TX;
+  P.tiles_y = (P.ny + C::TY - 1) / C::TY;
+  const int ntiles = P.tiles_x * P.tiles_y;
+  int chunks = L.chunks;
+  if (chunks <= 0) {
+    // pick the z-chunk count minimising waves x (planes + pipeline fill) per CTA
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::NTHREADS, C::SMEM);
+    const long resident = long(sms) * std::max(per, 1);
+    double best = 1e300;
+    chunks = 1;
+    for (int c = 1; c <= std::min(P.nz, 512); ++c) {
+      const int len = (P.nz + c - 1) / c;
+      if (c > 1 && (long(len) * (c - 1) >= P.nz))
+        continue; // would leave an empty chunk
+      const long units = long(ntiles) * c;
+      const long waves = (units + resident - 1) / resident;
+      const double cost = double(waves) * (len + 2 * C::R + 12);
+      if (cost < best - 1e-9) {
+        best = cost;
+        chunks = c;
+      }
+    }
+  }
+  P.chunk = (P.nz + chunks - 1) / chunks;
+  P.nchunks = (P.nz + P.chunk - 1) / P.chunk;
+  P.boundary_last = L.zorder_boundary_last;
+  P.out = static_cast<T *>(L.out);
+  P.w0 = fromBits<T>(s.w0);
+  for (int t = 0; t < 3; ++t) {
+    P.wz[t] = fromBits<T>(s.w[0][t]);
+    P.wy[t] = fromBits<T>(s.w[RANK == 3 ? 1 : 0][t]);
+    P.wx[t] = fromBits<T>(s.w[RANK - 1][t]);
+  }
+  P.scale = fromBits<T>(s.scale);
+  P.two = fromBits<T>(s.two);
+  const unsigned blocks = unsigned(ntiles) * unsigned(P.nchunks);
+  if (blocks_out)
+    *blocks_out = int(blocks);
+  kern<<<blocks, C::NTHREADS, C::SMEM, st>>>(*L.tm_cur, *L.tm_prev, P);
+  return cudaErr(cudaGetLastError(), "star kernel launch");
+}
+
+template <typename T, int RANK, int NT, int KIND> int residentT() {
+  using C = StarCfg<T, RANK, NT, KIND>;
+  auto kern = starKernel<T, RANK, NT, KIND>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::NTHREADS, C::SMEM);
+  return per;
+}
+
+template <typename T, int RANK> int dispatchNT(const StarLaunch &L, cudaStream_t st, int *b) {
+  const StarSpec &s = *L.spec;
+  if (s.kind == kHeat) {
+    if (s.ntaps == 1) return launchStarT<T, RANK, 1, kHeat>(L, st, b);
+    if (s.ntaps == 2) return launchStarT<T, RANK, 2, kHeat>(L, st, b);
+    if (s.ntaps == 3) return launchStarT<T, RANK, 3, kHeat>(L, st, b);
+  } else if (s.kind == kWave) {
+    if (s.ntaps == 1) return launchStarT<T, RANK, 1, kWave>(L, st, b);
+    if (s.ntaps == 2) return launchStarT<T, RANK, 2, kWave>(L, st, b);
+    if (s.ntaps == 3) return launchStarT<T, RANK, 3, kWave>(L, st, b);
+  }
+  return setError(HG_EUNSUPPORTED, "no star kernel for this tap set / kind");
+}
+
+template <typename T, int RANK> int residentNT(const StarSpec &s) {
+  if (s.kind == kHeat) {
+    if (s.ntaps == 1) return residentT<T, RANK, 1, kHeat>();
+    if (s.ntaps == 2) return residentT<T, RANK, 2, kHeat>();
+    if (s.ntaps == 3) return residentT<T, RANK, 3, kHeat>();
+  } else if (s.kind == kWave) {
+    if (s.ntaps == 1) return residentT<T, RANK, 1, kWave>();
+    if (s.ntaps == 2) return residentT<T, RANK, 2, kWave>();
+    if (s.ntaps == 3) return residentT<T, RANK, 3, kWave>();
+  }
+  return 0;
+}
+
+// ---- generic bytecode kernel --------------------------------------------------------------
+constexpr int kMaxSlots = 48;
+
+struct GenParams {
+  int rank, nops, noperands, nresults;
+  int64_t dom_lb[3], dom_ext[3];
+  int64_t npts;
+  const GOp *ops;
+  const void *op_base[HG_MAX_FIELDS];
+  DevLayout op_lay[HG_MAX_FIELDS];
+  void *out_base[HG_MAX_RESULTS];
+  DevLayout out_lay[HG_MAX_RESULTS];
+  int64_t st_lb[HG_MAX_RESULTS][3], st_ub[HG_MAX_RESULTS][3];
+  int res_slot[HG_MAX_RESULTS];
+};
+
+__device__ __forceinline__ int64_t layIndex(const DevLayout &L, const int64_t *p) {
+  // element index of logical point p in layout L
+  const int r = L.rank;
+  int64_t row = 0;
+  for (int d = 0; d < r - 1; ++d)
+    row = row * L.shape[d] + (p[d] - L.lb[d]);
+  return row * L.pitch + L.col0 + (p[r - 1] - L.lb[r - 1]);
+}
+
+template <typename T> __global__ void genericKernel(const __grid_constant__ GenParams P) {
+  T v[kMaxSlots];
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < P.npts;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t p[3] = {0, 0, 0};
+    int64_t rem = idx;
+    for (int d = P.rank - 1; d >= 0; --d) {
+      p[d] = P.dom_lb[d] + rem % P.dom_ext[d];
+      rem /= P.dom_ext[d];
+    }
+    int64_t base[HG_MAX_FIELDS];
+    for (int o = 0; o < P.noperands; ++o)
+      base[o] = layIndex(P.op_lay[o], p);
+    for (int i = 0; i < P.nops; ++i) {
+      const GOp op = P.ops[i];
+      switch (op.code) {
+      case HG_OP_ACCESS:
+        v[op.dst] = static_cast<const T *>(P.op_base[op.operand])[base[op.operand] + op.delta];
+        break;
+      case HG_OP_CONST:
+        v[op.dst] = fromBits<T>(op.bits);
+        break;
+      case HG_OP_ADD:
+        v[op.dst] = add_(v[op.a], v[op.b]);
+        break;
+      case HG_OP_SUB:
+        v[op.dst] = sub_(v[op.a], v[op.b]);
+        break;
+      case HG_OP_MUL:
+        v[op.dst] = mul_(v[op.a], v[op.b]);
+        break;
+      default:
+        v[op.dst] = div_(v[op.a], v[op.b]);
+        break;
+      }
+    }
+    for (int k = 0; k < P.nresults; ++k) {
+      bool in = true;
+      for (int d = 0; d < P.rank; ++d)
+        in = in && p[d] >= P.st_lb[k][d] && p[d] < P.st_ub[k][d];
+      if (in)
+        static_cast<T *>(P.out_base[k])[layIndex(P.out_lay[k], p)] = v[P.res_slot[k]];
+    }
+  }
+}
+
+// ---- initializer: exec::fillInit / initValue (buffer.cpp:142-179) ---------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+template <typename T>
+__global__ void initKernel(T *base, const DevLayout L, uint64_t seed, int64_t o0, int64_t o1,
+                           int64_t o2, int64_t total) {
+  const int r = L.rank;
+  const int64_t S = L.shape[r - 1];
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = i / S, j = i % S;
+    int64_t c[3];
+    int64_t rem = row;
+    for (int d = r - 2; d >= 0; --d) {
+      c[d] = L.lb[d] + rem % L.shape[d];
+      rem /= L.shape[d];
+    }
+    c[r - 1] = L.lb[r - 1] + j;
+    const int64_t org[3] = {o0, o1, o2};
+    uint64_t h = seed;
+    for (int d = 0; d < r; ++d)
+      h = mix64(h ^ static_cast<uint64_t>(c[d] + org[d]));
+    const double v = static_cast<double>(h >> 11) * 0x1.0p-53;
+    base[row * L.pitch + L.col0 + j] = static_cast<T>(v); // f32: cvt.rn.f32.f64
+  }
+}
+
+// ---- box copies -----------------------------------------------------------------------------
+template <typename T>
+__global__ void packKernel(T *base, const DevLayout L, int64_t a0, int64_t a1, int64_t a2,
+                           int64_t s0, int64_t s1, int64_t s2, T *packed, int unpack) {
+  // packRegion / unpackRegion (simulator.cpp:523-584): row-major over the box
+  const int64_t total = s0 * s1 * s2;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i2 = k % s2, i1 = (k / s2) % s1, i0 = k / (s1 * s2);
+    int64_t e;
+    if (L.rank == 3)
+      e = ((a0 + i0) * L.shape[1] + (a1 + i1)) * L.pitch + L.col0 + a2 + i2;
+    else if (L.rank == 2)
+      e = (a0 + i0) * L.pitch + L.col0 + a1 + i1;
+    else
+      e = L.col0 + a0 + i0;
+    if (unpack)
+      base[e] = packed[k];
+    else
+      packed[k] = base[e];
+  }
+}
+
+struct PutParams {
+  PutJob jobs[96];
+  int njobs;
+  DevLayout L;
+  unsigned long long *flags[2 * HG_MAX_RANK];
+  int nflags;
+  unsigned long long epoch;
+  unsigned int *counter;
+};
+
+__device__ __forceinline__ int64_t boxElem(const DevLayout &L, const int64_t *at, int64_t i0,
+                                           int64_t i1, int64_t i2) {
+  if (L.rank == 3)
+    return ((at[0] + i0) * L.shape[1] + (at[1] + i1)) * L.pitch + L.col0 + at[2] + i2;
+  if (L.rank == 2)
+    return (at[0] + i0) * L.pitch + L.col0 + at[1] + i1;
+  return L.col0 + at[0] + i0;
+}
+
+// Fused pack + NVLink store + unpack: each face box of my buffer is written straight into the
+// neighbour's receive box (peer-mapped), byte-exact.  The last CTA to finish publishes the
+// epoch to every neighbour's flag with a system-scope release.
+template <typename T> __global__ void putKernel(const __grid_constant__ PutParams P) {
+  const PutJob &J = P.jobs[blockIdx.y];
+  const int64_t rows = J.size[0] * (P.L.rank >= 2 ? J.size[1] : 1);
+  const int64_t w = P.L.rank == 3 ? J.size[2] : (P.L.rank == 2 ? J.size[1] : J.size[0]);
+  const int64_t rowsEff = P.L.rank == 1 ? 1 : rows;
+  const T *src = static_cast<const T *>(J.src);
+  T *dst = static_cast<T *>(J.dst);
+  for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
+    int64_t i0, i1;
+    if (P.L.rank == 3) {
+      i0 = r / J.size[1];
+      i1 = r % J.size[1];
+    } else {
+      i0 = r;
+      i1 = 0;
+    }
+    for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+      int64_t se, de;
+      if (P.L.rank == 3) {
+        se = boxElem(P.L, J.src_at, i0, i1, c);
+        de = boxElem(P.L, J.dst_at, i0, i1, c);
+      } else if (P.L.rank == 2) {
+        se = boxElem(P.L, J.src_at, i0, c, 0);
+        de = boxElem(P.L, J.dst_at, i0, c, 0);
+      } else {
+        se = boxElem(P.L, J.src_at, c, 0, 0);
+        de = boxElem(P.L, J.dst_at, c, 0, 0);
+      }
+      dst[de] = src[se];
+    }
+  }
+  if (P.nflags == 0)
+    return;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int total = gridDim.x * gridDim.y;
+    const unsigned int prev = atomicAdd(P.counter, 1u);
+    if (prev == total - 1) {
+      *P.counter = 0;
+      __threadfence_system();
+      for (int f = 0; f < P.nflags; ++f)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.flags[f]), "l"(P.epoch)
+                     : "memory");
+    }
+  }
+}
+
+__global__ void waitKernel(const unsigned long long *flags, int i0, int i1, int i2, int i3,
+                           int i4, int i5, int n, unsigned long long epoch) {
+  const int idx[6] = {i0, i1, i2, i3, i4, i5};
+  for (int k = 0; k < n; ++k) {
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + idx[k]) : "memory");
+    } while (v < epoch);
+  }
+  __threadfence_system();
+}
+
+} // namespace
+
+// ---- host wrappers ---------------------------------------------------------------------------
+
+int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay, void *base,
+                       CUtensorMap *cur, CUtensorMap *prev) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  static int loadErr = 0;
+  std::call_once(once, [&] {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      loadErr = 1;
+    else
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (loadErr)
+    return setError(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const int es = dtype == HG_F32 ? 4 : 8;
+  const int R = s.radius;
+  const int TX = (rank == 3 ? StarGeom<3>::TXT : StarGeom<2>::TXT) * 4;
+  const int TY = rank == 3 ? StarGeom<3>::TYT : 1;
+  const int RY = rank == 3 ? R : 0;
+  cuuint64_t dims[3], strides[2];
+  dims[0] = cuuint64_t(lay.pitch);
+  if (rank == 3) {
+    dims[1] = cuuint64_t(lay.shape[1]);
+    dims[2] = cuuint64_t(lay.shape[0]);
+    strides[0] = cuuint64_t(lay.pitch * es);
+    strides[1] = cuuint64_t(lay.pitch * lay.shape[1] * es);
+  } else {
+    dims[1] = 1;
+    dims[2] = cuuint64_t(lay.shape[0]);
+    strides[0] = cuuint64_t(lay.pitch * es);
+    strides[1] = cuuint64_t(lay.pitch * es);
+  }
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUtensorMapDataType dt =
+      dtype == HG_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  cuuint32_t boxCur[3] = {cuuint32_t(TX + 8), cuuint32_t(TY + 2 * RY), 1};
+  CUresult r = encode(cur, dt, 3, base, dims, strides, boxCur, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return setError(HG_ECUDA, "cuTensorMapEncodeTiled(cur) failed: " + std::to_string(int(r)));
+  cuuint32_t boxPrev[3] = {cuuint32_t(TX), cuuint32_t(TY), 1};
+  r = encode(prev, dt, 3, base, dims, strides, boxPrev, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return setError(HG_ECUDA, "cuTensorMapEncodeTiled(prev) failed: " + std::to_string(int(r)));
+  return HG_OK;
+}
+
+int launchStar(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
+  if (L.dtype == HG_F32)
+    return L.rank == 3 ? dispatchNT<float, 3>(L, st, blocks_out)
+                       : dispatchNT<float, 2>(L, st, blocks_out);
+  return L.rank == 3 ? dispatchNT<double, 3>(L, st, blocks_out)
+                     : dispatchNT<double, 2>(L, st, blocks_out);
+}
+
+int starResidentBlocks(const StarSpec &s, int dtype, int rank) {
+  if (dtype == HG_F32)
+    return rank == 3 ? residentNT<float, 3>(s) : residentNT<float, 2>(s);
+  return rank == 3 ? residentNT<double, 3>(s) : residentNT<double, 2>(s);
+}
+
+int launchGeneric(const GenericLaunch &L, cudaStream_t st) {
+  if (L.nslots > kMaxSlots)
+    return setError(HG_EUNSUPPORTED, "apply region needs more than " +
+                                         std::to_string(kMaxSlots) + " live values");
+  GenParams P{};
+  P.rank = L.rank;
+  P.nops = L.nops;
+  P.noperands = L.noperands;
+  P.nresults = L.nresults;
+  P.npts = 1;
+  for (int d = 0; d < L.rank; ++d) {
+    P.dom_lb[d] = L.dom_lb[d];
+    P.dom_ext[d] = L.dom_ext[d];
+    P.npts *= L.dom_ext[d];
+  }
+  P.ops = L.ops_dev;
+  for (int o = 0; o < L.noperands; ++o) {
+    P.op_base[o] = L.op_base[o];
+    P.op_lay[o] = L.op_lay[o];
+  }
+  for (int k = 0; k < L.nresults; ++k) {
+    P.out_base[k] = L.out_base[k];
+    P.out_lay[k] = L.out_lay[k];
+    P.res_slot[k] = L.res_slot[k];
+    for (int d = 0; d < 3; ++d) {
+      P.st_lb[k][d] = L.st_lb[k][d];
+      P.st_ub[k][d] = L.st_ub[k][d];
+    }
+  }
+  const int threads = 256;
+  const int64_t want = (P.npts + threads - 1) / threads;
+  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 32)));
+  if (L.dtype == HG_F32)
+    genericKernel<float><<<blocks, threads, 0, st>>>(P);
+  else
+    genericKernel<double><<<blocks, threads, 0, st>>>(P);
+  return cudaErr(cudaGetLastError(), "generic kernel launch");
+}
+
+int launchInit(void *base, const DevLayout &lay, int field, const int64_t *origin,
+               cudaStream_t st) {
+  int64_t total = 1;
+  for (int d = 0; d < lay.rank; ++d)
+    total *= lay.shape[d];
+  // seed = mix64(fieldIdx + 1), then one mix per coordinate (buffer.cpp:151-156)
+  uint64_t x = static_cast<uint64_t>(field) + 1;
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  const uint64_t seed = x ^ (x >> 31);
+  const int64_t o0 = origin ? origin[0] : 0, o1 = origin && lay.rank > 1 ? origin[1] : 0,
+                o2 = origin && lay.rank > 2 ? origin[2] : 0;
+  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256,
+                                                                          148 * 16)));
+  if (lay.es == 4)
+    initKernel<float><<<blocks, 256, 0, st>>>(static_cast<float *>(base), lay, seed, o0, o1, o2,
+                                              total);
+  else
+    initKernel<double><<<blocks, 256, 0, st>>>(static_cast<double *>(base), lay, seed, o0, o1,
+                                               o2, total);
+  return cudaErr(cudaGetLastError(), "init kernel launch");
+}
+
+int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,
+                     void *packed, int unpack, cudaStream_t st) {
+  int64_t a[3] = {0, 0, 0}, s[3] = {1, 1, 1};
+  for (int d = 0; d < lay.rank; ++d) {
+    a[d] = at[d];
+    s[d] = size[d];
+  }
+  // map to (s0,s1,s2) row-major with the last dim of the layout innermost
+  int64_t A0, A1, A2, S0, S1, S2;
+  if (lay.rank == 3) {
+    A0 = a[0]; A1 = a[1]; A2 = a[2]; S0 = s[0]; S1 = s[1]; S2 = s[2];
+  } else if (lay.rank == 2) {
+    A0 = a[0]; A1 = a[1]; A2 = 0; S0 = s[0]; S1 = s[1]; S2 = 1;
+  } else {
+    A0 = a[0]; A1 = 0; A2 = 0; S0 = s[0]; S1 = 1; S2 = 1;
+  }
+  const int64_t total = S0 * S1 * S2;
+  if (total <= 0)
+    return HG_OK;
+  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256,
+                                                                          148 * 16)));
+  if (lay.rank == 2) { // kernel indexes (a0+i0, a1+i1) via its rank-2 branch with s2 == 1
+    if (lay.es == 4)
+      packKernel<float><<<blocks, 256, 0, st>>>(static_cast<float *>(base), lay, A0, A1, 0, S0,
+                                                S1, 1, static_cast<float *>(packed), unpack);
+    else
+      packKernel<double><<<blocks, 256, 0, st>>>(static_cast<double *>(base), lay, A0, A1, 0,
+                                                 S0, S1, 1, static_cast<double *>(packed),
+                                                 unpack);
+  } else {
+    if (lay.es == 4)
+      packKernel<float><<<blocks, 256, 0, st>>>(static_cast<float *>(base), lay, A0, A1, A2, S0,
+                                                S1, S2, static_cast<float *>(packed), unpack);
+    else
+      packKernel<double><<<blocks, 256, 0, st>>>(static_cast<double *>(base), lay, A0, A1, A2,
+                                                 S0, S1, S2, static_cast<double *>(packed),
+                                                 unpack);
+  }
+  return cudaErr(cudaGetLastError(), "pack kernel launch");
+}
+
+int launchPut(const PutJob *jobs, int njobs, const DevLayout &lay, const PutSignal *sig, int nsig,
+              unsigned long long epoch, unsigned int *counter, cudaStream_t st) {
+  PutParams P{};
+  if (njobs > 96)
+    return setError(HG_EUNSUPPORTED, "too many exchange jobs in one swap phase");
+  for (int j = 0; j < njobs; ++j)
+    P.jobs[j] = jobs[j];
+  P.njobs = njobs;
+  P.L = lay;
+  P.nflags = 0;
+  for (int f = 0; f < nsig; ++f)
+    if (sig[f].flag)
+      P.flags[P.nflags++] = sig[f].flag;
+  P.epoch = epoch;
+  P.counter = counter;
+  if (njobs == 0 && P.nflags == 0)
+    return HG_OK;
+  int64_t maxRows = 1;
+  for (int j = 0; j < njobs; ++j) {
+    int64_t rows = lay.rank == 3 ? jobs[j].size[0] * jobs[j].size[1]
+                                 : (lay.rank == 2 ? jobs[j].size[0] : 1);
+    maxRows = std::max(maxRows, rows);
+  }
+  dim3 grid(unsigned(std::min<int64_t>(maxRows, 1184)), unsigned(std::max(njobs, 1)));
+  if (njobs == 0) { // flags only: a single CTA with no copy work
+    P.jobs[0] = PutJob{};
+    grid = dim3(1, 1);
+  }
+  if (lay.es == 4)
+    putKernel<float><<<grid, 256, 0, st>>>(P);
+  else
+    putKernel<double><<<grid, 256, 0, st>>>(P);
+  return cudaErr(cudaGetLastError(), "put kernel launch");
+}
+
+int launchWaitFlags(const unsigned long long *flags, const int *idx, int n,
+                    unsigned long long epoch, cudaStream_t st) {
+  if (n <= 0)
+    return HG_OK;
+  int i[6] = {0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < n && k < 6; ++k)
+    i[k] = idx[k];
+  waitKernel<<<1, 1, 0, st>>>(flags, i[0], i[1], i[2], i[3], i[4], i[5], n, epoch);
+  return cudaErr(cudaGetLastError(), "wait kernel launch");
+}
+
+} // namespace hg

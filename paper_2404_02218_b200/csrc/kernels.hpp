@@ -1,0 +1,85 @@
+// kernels.hpp -- launchers of the sm_100a kernels (kernels.cu) used by the host side.
+#ifndef HG_KERNELS_HPP
+#define HG_KERNELS_HPP
+
+#include "hg_internal.hpp"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace hg {
+
+// Device view of one buffer's layout (see makeLayout).
+struct DevLayout {
+  int64_t shape[3];
+  int64_t lb[3];
+  int64_t pitch;
+  int64_t col0;
+  int32_t rank;
+  int32_t es;
+};
+
+DevLayout devLayout(const Layout &L);
+
+// ---- star family (TMA-pipelined, register-streamed along dim 0) -------------------------
+struct StarLaunch {
+  const StarSpec *spec;
+  int dtype;
+  int rank;
+  // output region, raw indices in the (shared) layout
+  int64_t start[3];
+  int64_t ext[3];
+  DevLayout lay;
+  const CUtensorMap *tm_cur;  // tensor map of the buffer bound to the cur operand
+  const CUtensorMap *tm_prev; // wave: prev operand (may equal tm_cur otherwise)
+  void *out;                  // base of the output buffer allocation
+  int chunks;                 // z-chunks (0 = auto)
+  int zorder_boundary_last;   // process z-boundary chunks last (dmp overlap)
+};
+// Creates the TMA descriptor of a buffer for the star family's cur/prev boxes.
+int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay,
+                       void *base, CUtensorMap *cur, CUtensorMap *prev);
+int launchStar(const StarLaunch &L, cudaStream_t st, int *blocks_out);
+int starResidentBlocks(const StarSpec &s, int dtype, int rank);
+
+// ---- generic bytecode kernel ------------------------------------------------------------
+struct GenericLaunch {
+  int dtype, rank;
+  int64_t dom_lb[3], dom_ext[3];
+  int nops, nslots, noperands, nresults;
+  const GOp *ops_dev;
+  const void *op_base[HG_MAX_FIELDS];
+  DevLayout op_lay[HG_MAX_FIELDS];
+  void *out_base[HG_MAX_RESULTS];
+  DevLayout out_lay[HG_MAX_RESULTS];
+  int64_t st_lb[HG_MAX_RESULTS][3], st_ub[HG_MAX_RESULTS][3];
+  int res_slot[HG_MAX_RESULTS];
+};
+int launchGeneric(const GenericLaunch &L, cudaStream_t st);
+
+// ---- fields -----------------------------------------------------------------------------
+int launchInit(void *base, const DevLayout &lay, int field, const int64_t *origin,
+               cudaStream_t st);
+// box copy between a layout box and a packed array (dir 0 = pack, 1 = unpack)
+int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,
+                     void *packed, int unpack, cudaStream_t st);
+
+// ---- halo put (fused pack + NVLink store + unpack) + flags --------------------------------
+struct PutJob {
+  const void *src;    // my buffer base
+  void *dst;          // neighbour's buffer base (peer-mapped)
+  int64_t src_at[3];  // raw send box origin
+  int64_t dst_at[3];  // raw receive box origin in the neighbour
+  int64_t size[3];
+};
+struct PutSignal {
+  unsigned long long *flag; // neighbour's flag word (peer-mapped), null = none
+};
+int launchPut(const PutJob *jobs, int njobs, const DevLayout &lay, const PutSignal *sig,
+              int nsig, unsigned long long epoch, unsigned int *counter, cudaStream_t st);
+int launchWaitFlags(const unsigned long long *flags, const int *idx, int n,
+                    unsigned long long epoch, cudaStream_t st);
+
+} // namespace hg
+
+#endif

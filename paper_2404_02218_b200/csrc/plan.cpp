@@ -1,0 +1,405 @@
+// plan.cpp -- device-resident plans: field allocation in HBM, upload/download, device init,
+// and the runSerialStencil time loop (serial.cpp:57-88) over the sm_100a kernels.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <exception>
+
+namespace hg {
+
+int cudaCheck(cudaError_t e, const char *what) {
+  if (e == cudaSuccess)
+    return HG_OK;
+  return setError(HG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+// Linear-scan slot allocation for the generic kernel: a value lives until its last use.
+int compileGeneric(hg_plan &p) {
+  const hg_program &g = p.prog;
+  std::vector<int> last(static_cast<size_t>(g.nops), -1);
+  for (int i = 0; i < g.nops; ++i) {
+    const hg_op &o = g.ops[i];
+    if (o.code >= HG_OP_ADD) {
+      last[static_cast<size_t>(o.a)] = std::max(last[static_cast<size_t>(o.a)], i);
+      last[static_cast<size_t>(o.b)] = std::max(last[static_cast<size_t>(o.b)], i);
+    }
+  }
+  for (int k = 0; k < g.nresults; ++k)
+    last[static_cast<size_t>(g.result_op[k])] = g.nops;
+  std::vector<int> slot(static_cast<size_t>(g.nops), -1);
+  std::vector<int> freeSlots;
+  int nslots = 0;
+  std::vector<GOp> out(static_cast<size_t>(g.nops));
+  for (int i = 0; i < g.nops; ++i) {
+    const hg_op &o = g.ops[i];
+    GOp &q = out[static_cast<size_t>(i)];
+    std::memset(&q, 0, sizeof q);
+    q.code = o.code;
+    if (o.code >= HG_OP_ADD) {
+      q.a = static_cast<int16_t>(slot[static_cast<size_t>(o.a)]);
+      q.b = static_cast<int16_t>(slot[static_cast<size_t>(o.b)]);
+      // operands dying here free their slots before the result is assigned
+      for (int v : {o.a, o.b})
+        if (last[static_cast<size_t>(v)] == i && slot[static_cast<size_t>(v)] >= 0) {
+          if (std::find(freeSlots.begin(), freeSlots.end(), slot[static_cast<size_t>(v)]) ==
+              freeSlots.end())
+            freeSlots.push_back(slot[static_cast<size_t>(v)]);
+        }
+    }
+    int s;
+    if (!freeSlots.empty()) {
+      s = freeSlots.back();
+      freeSlots.pop_back();
+    } else {
+      s = nslots++;
+    }
+    slot[static_cast<size_t>(i)] = s;
+    q.dst = static_cast<int16_t>(s);
+    if (last[static_cast<size_t>(i)] < 0) // dead value: free immediately
+      freeSlots.push_back(s);
+    if (o.code == HG_OP_ACCESS) {
+      q.operand = static_cast<int16_t>(o.operand);
+      const Layout &L = p.lay[static_cast<size_t>(g.operand_field[o.operand])];
+      int64_t stride = 1, delta = 0;
+      for (int d = g.rank - 1; d >= 0; --d) {
+        delta += o.off[d] * stride;
+        stride *= d == g.rank - 1 ? L.pitch : L.shape[d];
+      }
+      q.delta = delta;
+    } else if (o.code == HG_OP_CONST) {
+      q.bits = o.bits;
+    }
+  }
+  p.nslots = nslots;
+  p.resSlot.clear();
+  for (int k = 0; k < g.nresults; ++k)
+    p.resSlot.push_back(slot[static_cast<size_t>(g.result_op[k])]);
+  int st = cudaCheck(cudaMalloc(&p.gopsDev, sizeof(GOp) * out.size()), "cudaMalloc(ops)");
+  if (st)
+    return st;
+  return cudaCheck(cudaMemcpy(p.gopsDev, out.data(), sizeof(GOp) * out.size(),
+                              cudaMemcpyHostToDevice),
+                   "cudaMemcpy(ops)");
+}
+
+} // namespace
+
+int planStep(hg_plan &p, cudaStream_t st) {
+  const hg_program &g = p.prog;
+  const Analysis &a = p.an;
+  if (a.family == Family::Star) {
+    const StarSpec &s = a.star;
+    const int bCur = p.bind[static_cast<size_t>(g.operand_field[s.cur_operand])];
+    const int bPrev =
+        s.kind == kWave ? p.bind[static_cast<size_t>(g.operand_field[s.prev_operand])] : bCur;
+    const int bOut = p.bind[static_cast<size_t>(g.store_field[0])];
+    StarLaunch L{};
+    L.spec = &s;
+    L.dtype = g.dtype;
+    L.rank = g.rank;
+    const Layout &lay = p.lay[static_cast<size_t>(bOut)];
+    for (int d = 0; d < g.rank; ++d) {
+      L.start[d] = g.store[0].lb[d] - lay.lb[d];
+      L.ext[d] = g.store[0].ub[d] - g.store[0].lb[d];
+    }
+    L.lay = devLayout(lay);
+    L.tm_cur = &p.tmCur[static_cast<size_t>(bCur)];
+    L.tm_prev = &p.tmPrev[static_cast<size_t>(bPrev)];
+    L.out = p.dptr[static_cast<size_t>(bOut)];
+    L.chunks = p.chunks;
+    L.zorder_boundary_last = p.boundaryLast;
+    int st2 = launchStar(L, st, nullptr);
+    if (st2)
+      return st2;
+  } else {
+    GenericLaunch L{};
+    L.dtype = g.dtype;
+    L.rank = g.rank;
+    for (int d = 0; d < g.rank; ++d) {
+      L.dom_lb[d] = a.dom_lb[d];
+      L.dom_ext[d] = a.dom_ub[d] - a.dom_lb[d];
+    }
+    L.nops = g.nops;
+    L.nslots = p.nslots;
+    L.noperands = g.noperands;
+    L.nresults = g.nresults;
+    L.ops_dev = p.gopsDev;
+    for (int o = 0; o < g.noperands; ++o) {
+      const int b = p.bind[static_cast<size_t>(g.operand_field[o])];
+      L.op_base[o] = p.dptr[static_cast<size_t>(b)];
+      L.op_lay[o] = devLayout(p.lay[static_cast<size_t>(b)]);
+    }
+    for (int k = 0; k < g.nresults; ++k) {
+      const int b = p.bind[static_cast<size_t>(g.store_field[k])];
+      L.out_base[k] = p.dptr[static_cast<size_t>(b)];
+      L.out_lay[k] = devLayout(p.lay[static_cast<size_t>(b)]);
+      L.res_slot[k] = p.resSlot[static_cast<size_t>(k)];
+      for (int d = 0; d < 3; ++d) {
+        L.st_lb[k][d] = d < g.rank ? g.store[k].lb[d] : 0;
+        L.st_ub[k][d] = d < g.rank ? g.store[k].ub[d] : 1;
+      }
+    }
+    int st2 = launchGeneric(L, st);
+    if (st2)
+      return st2;
+  }
+  ++p.launches;
+  // rotate (serial.cpp:83-85): next[i] = binding[src[i]]
+  std::vector<int> nxt(p.bind.size());
+  for (size_t i = 0; i < p.bind.size(); ++i)
+    nxt[i] = p.bind[static_cast<size_t>(a.src[i])];
+  p.bind.swap(nxt);
+  ++p.stepsDone;
+  return HG_OK;
+}
+
+} // namespace hg
+
+using namespace hg;
+
+#define HG_GUARD_BEGIN try {
+#define HG_GUARD_END                                                                          \
+  }                                                                                           \
+  catch (const std::exception &e) {                                                           \
+    return setError(HG_EINVAL, std::string("internal error: ") + e.what());                   \
+  }
+
+extern "C" {
+
+int hg_device_count(int *n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (n)
+    *n = e == cudaSuccess ? c : 0;
+  return e == cudaSuccess ? HG_OK : cudaCheck(e, "cudaGetDeviceCount");
+}
+
+int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
+  HG_GUARD_BEGIN
+  if (!prog || !out)
+    return setError(HG_EINVAL, "null argument");
+  *out = nullptr;
+  auto p = std::make_unique<hg_plan>();
+  p->prog = *prog;
+  p->ops.assign(prog->ops, prog->ops + std::max(prog->nops, 0));
+  p->prog.ops = p->ops.data();
+  int st = analyze(p->prog, p->an);
+  if (st)
+    return st;
+  const hg_program &g = p->prog;
+  // rotating buffers must share one layout (the kernel addresses a slot, not a buffer)
+  {
+    int at = 0;
+    for (int gi = 0; gi < g.ngroups; ++gi) {
+      for (int j = 1; j < g.group_len[gi]; ++j) {
+        const hg_bounds &x = g.fields[g.groups[at]], &y = g.fields[g.groups[at + j]];
+        for (int d = 0; d < g.rank; ++d)
+          if (x.lb[d] != y.lb[d] || x.ub[d] != y.ub[d])
+            return setError(HG_EUNSUPPORTED,
+                            "time-slot group rotates fields of different bounds");
+      }
+      at += g.group_len[gi];
+    }
+  }
+  p->device = device;
+  st = cudaCheck(cudaSetDevice(device), "cudaSetDevice");
+  if (st)
+    return st;
+  const int es = g.dtype == HG_F32 ? 4 : 8;
+  const int64_t coreLast = g.store[0].lb[g.rank - 1];
+  for (int f = 0; f < g.nfields; ++f) {
+    Layout L = makeLayout(g.fields[f], g.rank, es, coreLast);
+    void *ptr = nullptr;
+    st = cudaCheck(cudaMalloc(&ptr, L.bytes()), "cudaMalloc(field)");
+    if (st)
+      return st;
+    p->lay.push_back(L);
+    p->dptr.push_back(ptr);
+    st = cudaCheck(cudaMemset(ptr, 0, L.bytes()), "cudaMemset(field)");
+    if (st)
+      return st;
+  }
+  if (p->an.family == Family::Star && p->an.star.kind == kCopy)
+    p->an.family = Family::Generic; // a plain copy needs no stencil machinery
+  if (p->an.family == Family::Star) {
+    p->tmCur.resize(static_cast<size_t>(g.nfields));
+    p->tmPrev.resize(static_cast<size_t>(g.nfields));
+    for (int f = 0; f < g.nfields; ++f) {
+      st = makeStarTensorMaps(p->an.star, g.dtype, g.rank, devLayout(p->lay[static_cast<size_t>(f)]),
+                              p->dptr[static_cast<size_t>(f)], &p->tmCur[static_cast<size_t>(f)],
+                              &p->tmPrev[static_cast<size_t>(f)]);
+      if (st)
+        return st;
+    }
+  } else {
+    st = compileGeneric(*p);
+    if (st)
+      return st;
+    if (p->nslots > 48)
+      return setError(HG_EUNSUPPORTED, "apply region needs too many live values");
+  }
+  p->bind.resize(static_cast<size_t>(g.nfields));
+  for (int i = 0; i < g.nfields; ++i)
+    p->bind[static_cast<size_t>(i)] = i;
+  *out = p.release();
+  return HG_OK;
+  HG_GUARD_END
+}
+
+int hg_plan_destroy(hg_plan *p) {
+  if (!p)
+    return HG_OK;
+  cudaSetDevice(p->device);
+  for (void *d : p->dptr)
+    cudaFree(d);
+  if (p->gopsDev)
+    cudaFree(p->gopsDev);
+  delete p;
+  return HG_OK;
+}
+
+int hg_plan_kernel_name(const hg_plan *p, char *name, size_t cap) {
+  if (!p)
+    return setError(HG_EINVAL, "null plan");
+  std::string n = p->an.family == Family::Star
+                      ? p->an.name
+                      : "generic" + std::to_string(p->prog.rank) + "d_" +
+                            (p->prog.dtype == HG_F32 ? "f32" : "f64");
+  if (name && cap)
+    std::snprintf(name, cap, "%s", n.c_str());
+  return HG_OK;
+}
+
+int hg_plan_layout(const hg_plan *p, int b, hg_layout *out) {
+  if (!p || !out || b < 0 || b >= static_cast<int>(p->lay.size()))
+    return setError(HG_EINVAL, "bad plan/buffer");
+  const Layout &L = p->lay[static_cast<size_t>(b)];
+  std::memset(out, 0, sizeof *out);
+  out->rank = L.rank;
+  out->elem_bytes = L.es;
+  for (int d = 0; d < L.rank; ++d) {
+    out->shape[d] = L.shape[d];
+    out->lb[d] = L.lb[d];
+  }
+  out->pitch = L.pitch;
+  out->col0 = L.col0;
+  out->rows = L.rows;
+  out->device_ptr = p->dptr[static_cast<size_t>(b)];
+  return HG_OK;
+}
+
+int hg_plan_init_fields(hg_plan *p, const int64_t *origin, void *stream) {
+  if (!p)
+    return setError(HG_EINVAL, "null plan");
+  int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice");
+  if (st)
+    return st;
+  for (size_t b = 0; b < p->dptr.size(); ++b) {
+    // initialFields fills argument i with fieldIdx i (kernels.cpp:261-270)
+    st = launchInit(p->dptr[b], devLayout(p->lay[b]), static_cast<int>(b), origin,
+                    static_cast<cudaStream_t>(stream));
+    if (st)
+      return st;
+    ++p->launches;
+  }
+  return HG_OK;
+}
+
+static int copy2d(hg_plan *p, int b, void *host, size_t bytes, void *stream, bool up) {
+  if (!p || b < 0 || b >= static_cast<int>(p->lay.size()))
+    return setError(HG_EINVAL, "bad plan/buffer");
+  const Layout &L = p->lay[static_cast<size_t>(b)];
+  if (bytes != static_cast<size_t>(L.logicalCount()) * L.es)
+    return setError(HG_EINVAL, "host buffer size does not match the field");
+  int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice");
+  if (st)
+    return st;
+  const size_t w = static_cast<size_t>(L.shape[L.rank - 1]) * L.es;
+  char *dev = static_cast<char *>(p->dptr[static_cast<size_t>(b)]) + L.col0 * L.es;
+  const size_t dp = static_cast<size_t>(L.pitch) * L.es;
+  cudaError_t e =
+      up ? cudaMemcpy2DAsync(dev, dp, host, w, w, static_cast<size_t>(L.rows),
+                             cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream))
+         : cudaMemcpy2DAsync(host, w, dev, dp, w, static_cast<size_t>(L.rows),
+                             cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess && !up)
+    e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  return cudaCheck(e, up ? "upload" : "download");
+}
+
+int hg_plan_upload(hg_plan *p, int b, const void *host, size_t bytes, void *stream) {
+  return copy2d(p, b, const_cast<void *>(host), bytes, stream, true);
+}
+
+int hg_plan_download(hg_plan *p, int b, void *host, size_t bytes, void *stream) {
+  return copy2d(p, b, host, bytes, stream, false);
+}
+
+int hg_plan_run(hg_plan *p, int64_t steps, void *stream) {
+  if (!p)
+    return setError(HG_EINVAL, "null plan");
+  if (steps < 0)
+    return setError(HG_EINVAL, "negative step count");
+  int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice");
+  if (st)
+    return st;
+  for (int64_t t = 0; t < steps; ++t) {
+    st = planStep(*p, static_cast<cudaStream_t>(stream));
+    if (st)
+      return st;
+  }
+  return HG_OK;
+}
+
+int hg_plan_binding(const hg_plan *p, int32_t *perm, int64_t *steps_done) {
+  if (!p)
+    return setError(HG_EINVAL, "null plan");
+  if (perm)
+    for (size_t i = 0; i < p->bind.size(); ++i)
+      perm[i] = p->bind[i];
+  if (steps_done)
+    *steps_done = p->stepsDone;
+  return HG_OK;
+}
+
+int hg_plan_reset_binding(hg_plan *p) {
+  if (!p)
+    return setError(HG_EINVAL, "null plan");
+  for (size_t i = 0; i < p->bind.size(); ++i)
+    p->bind[i] = static_cast<int>(i);
+  p->stepsDone = 0;
+  return HG_OK;
+}
+
+static int packImpl(hg_plan *p, int b, const int64_t *at, const int64_t *size, void *dev,
+                    void *stream, int unpack) {
+  if (!p || b < 0 || b >= static_cast<int>(p->lay.size()) || !at || !size || !dev)
+    return setError(HG_EINVAL, "bad pack arguments");
+  const Layout &L = p->lay[static_cast<size_t>(b)];
+  for (int d = 0; d < L.rank; ++d)
+    if (at[d] < 0 || size[d] < 0 || at[d] + size[d] > L.shape[d])
+      return setError(HG_ETRAP, "exchange region escapes the buffer");
+  int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice");
+  if (st)
+    return st;
+  ++p->launches;
+  return launchPackUnpack(p->dptr[static_cast<size_t>(b)], devLayout(L), at, size, dev, unpack,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int hg_plan_pack(hg_plan *p, int b, const int64_t *at, const int64_t *size, void *dst,
+                 void *stream) {
+  return packImpl(p, b, at, size, dst, stream, 0);
+}
+
+int hg_plan_unpack(hg_plan *p, int b, const int64_t *at, const int64_t *size, const void *src,
+                   void *stream) {
+  return packImpl(p, b, at, size, const_cast<void *>(src), stream, 1);
+}
+
+int64_t hg_plan_launch_count(const hg_plan *p) { return p ? p->launches : 0; }
+
+} // extern "C"

@@ -1,0 +1,34 @@
+// plan.hpp -- the hg_plan object (internal).
+#ifndef HG_PLAN_HPP
+#define HG_PLAN_HPP
+
+#include "kernels.hpp"
+
+#include <memory>
+#include <vector>
+
+struct hg_plan {
+  int device = 0;
+  hg_program prog{};
+  std::vector<hg_op> ops;
+  hg::Analysis an;
+  std::vector<hg::Layout> lay;        // per buffer (initial argument index)
+  std::vector<void *> dptr;           // per buffer
+  std::vector<CUtensorMap> tmCur, tmPrev;
+  std::vector<int> bind;              // slot -> buffer
+  int64_t stepsDone = 0;
+  hg::GOp *gopsDev = nullptr;
+  int nslots = 0;
+  std::vector<int> resSlot;
+  int64_t launches = 0;
+  int chunks = 0;                     // star z-chunks (0 = auto)
+  int boundaryLast = 0;               // star: z-boundary chunks last (dmp overlap)
+};
+
+namespace hg {
+int cudaCheck(cudaError_t e, const char *what);
+// One time step on `st` with the current binding, then rotate.
+int planStep(hg_plan &p, cudaStream_t st);
+} // namespace hg
+
+#endif

@@ -1,0 +1,129 @@
+"""Host side of the C-ABI (no GPU): the library loads and exports every symbol of
+include/hg/hg.h; the program builder, decompose pass, dmp arithmetic, initializer and binding
+rotation reproduce the reference's own outputs (tests/golden/) exactly; errors are loud."""
+import ctypes as C
+import struct
+
+import numpy as np
+import pytest
+
+import paper_2404_02218_b200 as hg
+from paper_2404_02218_b200 import _capi as capi
+from helpers import decomp_to_json, program_from_json, prog_to_json
+
+
+def test_library_exports_every_declared_symbol():
+    L = capi.lib()
+    names = capi.exported_symbols()
+    assert len(names) >= 35
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_builder_matches_reference_modules(golden):
+    # exec::buildKernel (kernels.cpp:139-243) re-read from the reference module, op by op,
+    # including the f32 constant bits of the retyped module
+    for c in golden["serial"]:
+        k, r, e, o, f32 = c["spec"]
+        p = hg.Program.build(hg.KernelSpec(k, r, e, o, "f32" if f32 else "f64"))
+        assert prog_to_json(p) == c["program"], c["spec"]
+
+
+def test_f32_constant_bits_from_survey():
+    p = hg.Program.build(hg.KernelSpec("wave", 3, 16, 8, "f32"))
+    bits = [o.bits for o in p.op_list() if o.code == capi.HG_OP_CONST]
+    assert {0xc0fc0000, 0x3fb60b61, 0xbde38e39, 0x3ab60b61, 0x40000000, 0x3c23d70a} == set(bits)
+    p = hg.Program.build(hg.KernelSpec("heat", 3, 16, 4, "f32"))
+    bits = {o.bits for o in p.op_list() if o.code == capi.HG_OP_CONST}
+    assert bits == {0xc0f00000, 0x3faaaaab, 0xbdaaaaab, 0x3c23d70a}
+
+
+def test_decompose_matches_reference(golden):
+    # the decompose pass (dmp_transforms.cpp:101-312): local field bounds, stores, swaps
+    for c in golden["decomposed"]:
+        k, r, e, o, f32 = c["spec"]
+        p = hg.Program.build(hg.KernelSpec(k, r, e, o, "f32" if f32 else "f64"))
+        local, dc = p.decompose(c["grid"])
+        assert prog_to_json(local) == c["local_program"], c["spec"]
+        assert decomp_to_json(dc) == c["decomp"], c["spec"]
+
+
+def test_decompose_rejects_what_the_reference_rejects():
+    p = hg.Program.build(hg.KernelSpec("heat", 2, 10, 2, "f32"))
+    with pytest.raises(capi.HgError, match="not divisible"):
+        p.decompose([3, 1])
+    with pytest.raises(capi.HgError, match="grid rank"):
+        p.decompose([2])
+    p = hg.Program.build(hg.KernelSpec("heat", 2, 4, 8, "f32"))
+    with pytest.raises(capi.HgError, match="halo width exceeds"):
+        p.decompose([2, 2])
+
+
+def test_exchanges_neighbors_slicing_binding(golden):
+    for x in golden["dmp"]["exchanges"]:
+        got = hg.exchanges(x["core"], x["below"], x["above"], x["grid"], x["coord"])
+        want = [{"at": d[0], "size": d[1], "offset": d[2], "to": d[3]} for d in x["decls"]]
+        assert got == want
+    for n in golden["dmp"]["neighbors"]:
+        assert hg.neighbor_rank(n["rank"], n["dir"], n["grid"]) == n["nbr"]
+    for c in golden["dmp"]["coords"]:
+        assert hg.coord_from_rank(c["rank"], c["grid"]) == c["coord"]
+        assert hg.rank_from_coord(c["coord"], c["grid"]) == c["rank"]
+    for ext, parts, p, lb, ub in golden["dmp"]["slicing"]:
+        assert hg.local_interval(ext, parts, p) == (lb, ub)
+    for b in golden["binding_after"]:
+        assert hg.binding_after(b["groups"], b["nargs"], b["steps"]) == b["perm"]
+
+
+def test_init_value_and_fingerprint(golden):
+    for iv in golden["init_values"]:
+        v = hg.init_value(iv["field"], iv["coord"])
+        assert struct.pack("<d", v).hex() == iv["f64"]
+    assert hg.fingerprint(np.zeros(0, np.uint8)) == 0xcbf29ce484222325
+    assert hg.fingerprint(np.frombuffer(b"a", np.uint8)) == 0xaf63dc4c8601ec8c  # FNV-1a("a")
+
+
+def test_kernel_family_matching(golden):
+    fam = {}
+    for c in golden["serial"]:
+        k, r, e, o, f32 = c["spec"]
+        p = hg.Program.build(hg.KernelSpec(k, r, e, o, "f32" if f32 else "f64"))
+        fam[(k, r, o, f32)] = p.kernel_family()
+    assert fam[("heat", 3, 4, 1)] == "star3d_r2_heat_f32"
+    assert fam[("wave", 3, 8, 1)] == "star3d_r4_wave_f32"
+    assert fam[("heat", 2, 2, 1)] == "star2d_r1_heat_f32"
+    assert fam[("heat", 3, 8, 0)] == "star3d_r4_heat_f64"
+    assert fam[("heat", 1, 2, 1)] == "generic1d_f32"
+    for c in golden["authored"]:
+        assert program_from_json(c["program"]).kernel_family().startswith("generic")
+
+
+def test_validation_errors():
+    p = hg.Program.build(hg.KernelSpec("heat", 2, 8, 2, "f32"))
+    p.prog.ops[5].a = 7  # use before def
+    with pytest.raises(capi.HgError, match="use before def"):
+        p.kernel_family()
+    p = hg.Program.build(hg.KernelSpec("heat", 2, 8, 2, "f32"))
+    p.prog.ops[3].off[0] = 5  # reaches past the halo
+    with pytest.raises(capi.HgError, match="escapes"):
+        p.kernel_family()
+    with pytest.raises(capi.HgError, match="unknown kernel"):
+        hg.Program.build(hg.KernelSpec("nope", 2, 8, 2))
+    with pytest.raises(capi.HgError, match="order"):
+        hg.Program.build(hg.KernelSpec("heat", 2, 8, 3))
+
+
+def test_plan_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    p = hg.Program.build(hg.KernelSpec("heat", 2, 8, 2, "f32"))
+    with pytest.raises(capi.HgError) as e:
+        hg.Plan(p)
+    assert e.value.status == capi.HG_ECUDA
+
+
+def test_csv_and_throughput():
+    assert hg.csv_header() == "label,core_points,steps,seconds,gpts_per_s"
+    assert hg.gpts_per_sec(10**9, 2, 4.0) == 0.5
+    assert hg.csv_row("x", 100, 2, 0.5).startswith("x,100,2,0.5,")
