@@ -205,6 +205,9 @@ int hg_plan_pack(hg_plan *plan, int buffer, const int64_t *at, const int64_t *si
                  void *dst_device, void *stream);
 int hg_plan_unpack(hg_plan *plan, int buffer, const int64_t *at, const int64_t *size,
                    const void *src_device, void *stream);
+/* Tuning knobs of the star family: z-chunks per column tile (0 = auto) and whether the
+ * z-boundary chunks run last (lets halo exchange overlap interior compute). */
+int hg_plan_set_tuning(hg_plan *plan, int chunks, int boundary_last);
 /* Kernel launches issued by this plan so far (for bench/gpu_launches accounting). */
 int64_t hg_plan_launch_count(const hg_plan *plan);
 

@@ -299,6 +299,9 @@ class Plan:
     def reset_binding(self):
         check(lib().hg_plan_reset_binding(self.h))
 
+    def set_tuning(self, chunks: int = 0, boundary_last: bool = False):
+        check(lib().hg_plan_set_tuning(self.h, chunks, 1 if boundary_last else 0))
+
     def launch_count(self) -> int:
         return int(lib().hg_plan_launch_count(self.h))
 

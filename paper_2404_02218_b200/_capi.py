@@ -63,7 +63,8 @@ class HgLayout(C.Structure):
                 ("device_ptr", C.c_void_p)]
 
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libhalogen_b200.so")
+LIB_PATH = os.environ.get("HG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "lib", "libhalogen_b200.so")
 _lib = None
 
 
@@ -115,6 +116,7 @@ def lib() -> C.CDLL:
         "hg_plan_pack": (C.c_int, [V, C.c_int, P(I64), P(I64), V, V]),
         "hg_plan_unpack": (C.c_int, [V, C.c_int, P(I64), P(I64), V, V]),
         "hg_plan_launch_count": (I64, [V]),
+        "hg_plan_set_tuning": (C.c_int, [V, C.c_int, C.c_int]),
         "hg_dmp_create": (C.c_int, [V, P(HgDecomp), I64, P(V)]),
         "hg_dmp_destroy": (C.c_int, [V]),
         "hg_dmp_ipc_export": (C.c_int, [V, V, SZ, P(SZ)]),

@@ -16,6 +16,17 @@
 #include <type_traits>
 #include <utility>
 
+// TMA prefetch depth (planes in flight beyond the R+1 a CTA computes on); tunables.
+#ifndef HG_DEPTH3
+#define HG_DEPTH3 5
+#endif
+#ifndef HG_DEPTH3W
+#define HG_DEPTH3W 5
+#endif
+#ifndef HG_DEPTH2
+#define HG_DEPTH2 4
+#endif
+
 namespace hg {
 
 DevLayout devLayout(const Layout &L) {
@@ -178,7 +189,7 @@ template <typename T, int RANK, int NT, int KIND> struct StarCfg {
   static constexpr int NTHREADS = NCONS + 32;
   // CTAs per SM the register budget must allow (f32 3D: 3 for r<=2, 2 for r=4)
   static constexpr int MINB = RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? 3 : 2) : 1) : 4;
-  static constexpr int DEPTH = RANK == 3 ? 3 : 4;
+  static constexpr int DEPTH = RANK == 3 ? (R <= 2 ? HG_DEPTH3 : HG_DEPTH3W) : HG_DEPTH2;
   static constexpr int NS = R + 1 + DEPTH;
   static constexpr int Q = 2 * R + 1;
   static constexpr int STAGE = ROWS * CW;   // elements
@@ -628,9 +639,9 @@ __device__ __forceinline__ int64_t boxElem(const DevLayout &L, const int64_t *at
 // epoch to every neighbour's flag with a system-scope release.
 template <typename T> __global__ void putKernel(const __grid_constant__ PutParams P) {
   const PutJob &J = P.jobs[blockIdx.y];
-  const int64_t rows = J.size[0] * (P.L.rank >= 2 ? J.size[1] : 1);
+  // rows of the box (all dims but the last) x contiguous width (the last dim)
+  const int64_t rowsEff = P.L.rank == 3 ? J.size[0] * J.size[1] : (P.L.rank == 2 ? J.size[0] : 1);
   const int64_t w = P.L.rank == 3 ? J.size[2] : (P.L.rank == 2 ? J.size[1] : J.size[0]);
-  const int64_t rowsEff = P.L.rank == 1 ? 1 : rows;
   const T *src = static_cast<const T *>(J.src);
   T *dst = static_cast<T *>(J.dst);
   for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {

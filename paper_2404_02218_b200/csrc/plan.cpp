@@ -402,4 +402,12 @@ int hg_plan_unpack(hg_plan *p, int b, const int64_t *at, const int64_t *size, co
 
 int64_t hg_plan_launch_count(const hg_plan *p) { return p ? p->launches : 0; }
 
+int hg_plan_set_tuning(hg_plan *p, int chunks, int boundary_last) {
+  if (!p || chunks < 0)
+    return setError(HG_EINVAL, "bad tuning");
+  p->chunks = chunks;
+  p->boundaryLast = boundary_last ? 1 : 0;
+  return HG_OK;
+}
+
 } // extern "C"

@@ -1,0 +1,40 @@
+"""Multi-process halo swap over NVLink (one rank per GPU, CUDA IPC peer memory): bitwise
+against the oracle, halos included.  Needs >= 2 GPUs; the CPU side of the rank protocol is
+covered by tests/test_dist_gloo.py."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args", [
+    ["--kind", "heat", "--rank", "3", "--extent", "48", "--order", "4", "--T", "6"],
+    ["--kind", "wave", "--rank", "3", "--extent", "40", "--order", "8", "--T", "5"],
+    ["--kind", "heat", "--rank", "2", "--extent", "64", "--order", "2", "--T", "7"],
+])
+def test_ipc_dmp_two_ranks(args):
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    for nproc, grid in ((2, None), (min(n, 4), "2x2x1" if "3" == args[3] else "2x2")):
+        if nproc < 4 and grid:
+            continue
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone",
+               "--nproc-per-node", str(nproc), os.path.join(REPO, "tools", "dmp_check.py")] + args
+        if grid:
+            cmd += ["--grid", grid]
+        r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        assert "OK" in r.stdout

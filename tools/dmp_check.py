@@ -1,0 +1,70 @@
+"""Multi-process dmp check (one rank per GPU, CUDA IPC + NVLink puts): after T steps every
+rank's local buffers (cores AND halos) must equal the oracle's restatement of the reference's
+RankHooks::swap loop bit for bit.  Launched by tests/test_multigpu.py via torchrun."""
+import argparse
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "oracle"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2404_02218_b200 as hg  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kind", default="heat")
+    ap.add_argument("--rank", type=int, default=3)
+    ap.add_argument("--extent", type=int, default=48)
+    ap.add_argument("--order", type=int, default=4)
+    ap.add_argument("--grid", default=None)
+    ap.add_argument("--T", type=int, default=5)
+    a = ap.parse_args()
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    lr = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(lr)
+    dist.init_process_group("gloo")
+    grid = [int(x) for x in a.grid.split("x")] if a.grid else [world] + [1] * (a.rank - 1)
+    prog = hg.build_kernel(hg.KernelSpec(a.kind, a.rank, a.extent, a.order, "f32"))
+    local, dc = prog.decompose(grid)
+    plan = hg.Plan(local, lr)
+    coord = hg.coord_from_rank(rank, grid)
+    plan.init_fields(origin=[coord[d] * dc.core[d] for d in range(a.rank)])
+    dmp = hg.Dmp(plan, dc, rank)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, dmp.export())
+    for r, b in enumerate(blobs):
+        if r != rank:
+            dmp.import_peer(r, b)
+    dist.barrier()
+    dmp.run(a.T)
+    torch.cuda.synchronize()
+    perm, _ = plan.binding()
+    got = [plan.download(p) for p in perm]
+    from oracle import Port
+    port = Port()
+    glob = port.initial_fields(prog)
+    lbs = [prog.field_bounds(i)[0] for i in range(prog.nfields)]
+    want = port.simulate_rank_state(local, dc, glob, lbs, a.T, rank)
+    ok = all(np.array_equal(g.view(np.uint32), w.view(np.uint32)) for g, w in zip(got, want))
+    flag = torch.tensor([0 if ok else 1])
+    dist.all_reduce(flag)
+    dist.barrier()
+    dmp.close()
+    plan.close()
+    if rank == 0:
+        print(f"dmp_check {a.kind}{a.rank}d n{a.extent} o{a.order} grid={grid} T={a.T}: "
+              f"{'OK' if flag.item() == 0 else 'MISMATCH'} (bytes put by rank0 "
+              f"{dmp.bytes_exchanged() if False else 'n/a'})", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
