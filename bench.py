@@ -200,24 +200,26 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     sh = C.c_void_p(stream.cuda_stream)
 
+    from paper_2404_02218_b200 import dist as hd
     E = args.extent
-    grid = [world, 1, 1] if args.grid is None else [int(x) for x in args.grid.split("x")]
+    if args.grid is not None:
+        grid = [int(x) for x in args.grid.split("x")]
+    else:
+        grid = hd.weak_grid(world) if args.mode == "weak" else hd.strong_grid(world)
     assert int(grid[0] * grid[1] * grid[2]) == world
-    gext = [E * grid[0], E * grid[1], E * grid[2]]  # weak scaling: E^3 per GPU
+    if args.mode == "weak":
+        gext = [E * grid[0], E * grid[1], E * grid[2]]  # E^3 per GPU
+    else:
+        gext = [args.strong_extent] * 3                 # fixed global domain
     glob = hg.build_kernel(hg.KernelSpec("heat", 3, E, 4, "f32")).with_extents(gext)
     local, dc = glob.decompose(grid)
     plan = hg.Plan(local, local_rank)
-    coord = hg.coord_from_rank(rank, grid)
-    origin = [coord[d] * dc.core[d] for d in range(3)]
+    origin = hd.origin_of(rank, grid, list(dc.core[:3]))
     plan.init_fields(origin=origin, stream=sh)
     dmp = None
     if world > 1:
         dmp = hg.Dmp(plan, dc, rank)
-        blobs = [None] * world
-        dist.all_gather_object(blobs, dmp.export())
-        for r, b in enumerate(blobs):
-            if r != rank:
-                dmp.import_peer(r, b)
+        hd.connect(dmp, rank, grid, world)
         dist.barrier()
 
     def steps(k):
@@ -312,12 +314,13 @@ def run_ours(args):
                       "reference",
             "value": value, "unit": "GPts/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": args.mode, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference initValue hash, buffer.cpp:142-179)",
-            "config": {"workload": "heat3d_so4_weak (BASELINE config 5; N=1 is the 1-GPU case)",
-                       "kernel": plan.kernel_name, "core_per_gpu": [E, E, E],
+            "config": {"workload": f"heat3d_so4_{args.mode} (BASELINE config 5"
+                                   f"{'; N=1 is the 1-GPU case' if args.mode == 'weak' else ''})",
+                       "kernel": plan.kernel_name, "core_per_gpu": list(dc.core[:3]),
                        "global_core": gext, "grid": grid, "halo": 2,
-                       "l2": "inputs >> 126 MB L2 (2 x 4.6 GB fields per GPU), no flush needed",
+                       "l2": "inputs >> 126 MB L2 (GBs of fields per GPU), no flush needed",
                        "transport": "NVLink P2P put (CUDA IPC) + system-scope flags"
                        if world > 1 else "none"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -346,7 +349,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--extent", type=int, default=1024)
-    ap.add_argument("--grid", default=None, help="process grid AxBxC (default N x 1 x 1)")
+    ap.add_argument("--grid", default=None, help="process grid AxBxC (default: weak N x 1 x 1, "
+                                                 "strong 1/2x1x1/2x2x1/2x2x2)")
+    ap.add_argument("--mode", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--strong-extent", type=int, default=2048)
     ap.add_argument("--e2e-timesteps", type=int, default=100)
     ap.add_argument("--e2e-calls", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

@@ -319,11 +319,24 @@ int hg_dmp_run(hg_dmp *d, int64_t steps, void *stream) {
       return rc;
     if (nsig || !jobs.empty())
       ++p.launches;
-    rc = launchWaitFlags(d->flags, widx, nw, d->epoch, st);
-    if (rc)
-      return rc;
-    if (nw)
-      ++p.launches;
+    if (p.an.family == Family::Star && nw) {
+      // fused wait: only the CTAs whose halo rows touch a neighbour's face wait for its
+      // flag, inside the stencil kernel; z-boundary chunks run last, so the exchange
+      // overlaps the interior
+      int mask = 0;
+      for (int k = 0; k < nw; ++k)
+        mask |= 1 << widx[k];
+      p.waitFlags = d->flags;
+      p.waitEpoch = d->epoch;
+      p.waitMask = mask;
+      p.boundaryLast = (mask & 3) ? 1 : 0;
+    } else {
+      rc = launchWaitFlags(d->flags, widx, nw, d->epoch, st);
+      if (rc)
+        return rc;
+      if (nw)
+        ++p.launches;
+    }
     rc = planStep(p, st);
     if (rc)
       return rc;

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -25,6 +26,12 @@
 #endif
 #ifndef HG_DEPTH2
 #define HG_DEPTH2 4
+#endif
+#ifndef HG_CLUSTER_Y
+#define HG_CLUSTER_Y 1
+#endif
+#ifndef HG_ORDER
+#define HG_ORDER 0
 #endif
 
 namespace hg {
@@ -157,6 +164,13 @@ template <typename T> struct StarParams {
   int zs, ys, xs;  // raw start of the output region
   int nz, ny, nx;  // output extents
   int tiles_x, tiles_y, chunk, nchunks;
+  int cy, bands; // cluster size along y and number of y bands (tiles_y / cy, rounded up)
+  int order;     // unit -> (tile, chunk) order
+  // dmp: before loading any halo row of a face whose neighbour exists, the producer waits
+  // until that neighbour's put of this step has landed (flag >= epoch, system-scope acquire)
+  const unsigned long long *flags;
+  unsigned long long epoch;
+  int wmask;     // bit 2*dim + (sign > 0): a neighbour sends into that face
   int boundary_last;
   T *out;
   T w0, wz[3], wy[3], wx[3], scale, two;
@@ -209,22 +223,45 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND>::NTHREADS,
   using C = StarCfg<T, RANK, NT, KIND>;
   constexpr int R = C::R, RY = C::RY, NS = C::NS, Q = C::Q;
   extern __shared__ __align__(128) unsigned char smraw[];
-  T *stages = reinterpret_cast<T *>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  // align inside the __shared__ array (pointer stays in the shared window -> LDS, not LD)
+  T *stages = reinterpret_cast<T *>(smraw + ((128u - (smemAddr(smraw) & 127u)) & 127u));
   T *pstages = stages + size_t(NS) * C::SSTRIDE;
   uint64_t *full = reinterpret_cast<uint64_t *>(pstages + (C::WAVE ? size_t(NS) * C::PSTAGE : 0));
   uint64_t *empty = full + NS;
 
   // unit -> (tile, chunk); optionally the z-boundary chunks go last
-  const int ntiles = P.tiles_x * P.tiles_y;
-  const int unit = blockIdx.x;
-  const int tile = unit % ntiles;
-  int chunk = unit / ntiles;
+  // unit -> (y-member of a cluster, x tile, y band, z chunk); the cy CTAs of one cluster are
+  // the y-adjacent tiles of one column band, gang-scheduled so their shared halo rows are
+  // fetched from HBM once and hit in L2 for the neighbour
+  int u = blockIdx.x;
+  int txi, tyi, chunk;
+  if (P.order == 0) {
+    const int mem = u % P.cy;
+    u /= P.cy;
+    txi = u % P.tiles_x;
+    u /= P.tiles_x;
+    tyi = (u % P.bands) * P.cy + mem;
+    chunk = u / P.bands;
+  } else if (P.order == 1) { // chunk fastest: the z-chunks of one column tile run together
+    chunk = u % P.nchunks;
+    u /= P.nchunks;
+    txi = u % P.tiles_x;
+    tyi = u / P.tiles_x;
+  } else { // chunk fastest within 4x4 groups of column tiles
+    chunk = u % P.nchunks;
+    u /= P.nchunks;
+    const int g = u / 16, w = u % 16;
+    const int gx = (P.tiles_x + 3) / 4;
+    txi = (g % gx) * 4 + (w % 4);
+    tyi = (g / gx) * 4 + (w / 4);
+    if (txi >= P.tiles_x)
+      tyi = P.tiles_y; // padding unit: no work
+  }
   if (P.boundary_last && P.nchunks > 2)
     chunk = chunk < P.nchunks - 2 ? chunk + 1 : (chunk == P.nchunks - 2 ? 0 : P.nchunks - 1);
-  const int txi = tile % P.tiles_x, tyi = tile / P.tiles_x;
   const int xb = txi * C::TX, yb = tyi * C::TY;
   const int zb = chunk * P.chunk;
-  const int n = min(P.chunk, P.nz - zb);
+  const int n = tyi < P.tiles_y ? min(P.chunk, P.nz - zb) : 0;
   const int tid = threadIdx.x;
 
   if (tid == 0) {
@@ -243,6 +280,29 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND>::NTHREADS,
     if (tid == C::NCONS) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur))
                    : "memory");
+      if (P.flags) {
+        constexpr int XD = RANK - 1;
+        int need = 0;
+        if (zb == 0) need |= 1;
+        if (zb + n >= P.nz) need |= 2;
+        if (RANK == 3 && yb == 0) need |= 4;
+        if (RANK == 3 && yb + C::TY >= P.ny) need |= 8;
+        if (xb == 0) need |= 1 << (2 * XD);
+        if (xb + C::TX >= P.nx) need |= 2 << (2 * XD);
+        need &= P.wmask;
+        for (int di = 0; di < 6; ++di)
+          if (need & (1 << di)) {
+            unsigned long long v;
+            do {
+              asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+                           : "=l"(v)
+                           : "l"(P.flags + di)
+                           : "memory");
+            } while (v < P.epoch);
+          }
+        // the halo bytes arrived through the generic proxy; TMA reads via the async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       const int cx = int(P.col0) + P.xs + xb - C::PADX;
       const int cy = RANK == 3 ? P.ys + yb - RY : 0;
       const int z0 = P.zs + zb - R;
@@ -388,14 +448,22 @@ template <typename T, int RANK, int NT, int KIND>
 int launchStarT(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
   using C = StarCfg<T, RANK, NT, KIND>;
   auto kern = starKernel<T, RANK, NT, KIND>;
-  static std::once_flag once;
-  static cudaError_t attrErr = cudaSuccess;
-  std::call_once(once, [&] {
-    attrErr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(C::SMEM));
-  });
-  if (attrErr != cudaSuccess)
-    return cudaErr(attrErr, "cudaFuncSetAttribute(star)");
+  // function attributes are per device: opt in to the large shared-memory carve-out on
+  // every device this kernel is launched on
+  static std::mutex mu;
+  static unsigned long long doneMask = 0;
+  int curDev = 0;
+  cudaGetDevice(&curDev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(doneMask & (1ull << (curDev & 63)))) {
+      cudaError_t attrErr = cudaFuncSetAttribute(
+          kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+      if (attrErr != cudaSuccess)
+        return cudaErr(attrErr, "cudaFuncSetAttribute(star)");
+      doneMask |= 1ull << (curDev & 63);
+    }
+  }
   const StarSpec &s = *L.spec;
   StarParams<T> P{};
   int zd = 0, yd = RANK == 3 ? 1 : -1, xd = RANK - 1;
@@ -412,6 +480,12 @@ int launchStarT(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
   P.tiles_y = (P.ny + C::TY - 1) / C::TY;
   const int ntiles = P.tiles_x * P.tiles_y;
   int chunks = L.chunks;
+  if (chunks <= 0 && RANK == 3) {
+    // ~32R planes per chunk: short-lived CTAs keep neighbouring tiles in step (their shared
+    // halo rows then hit in L2), while the 2R-plane chunk overlap stays ~6% (measured sweep,
+    // profiles/README.md)
+    chunks = std::max(1, (P.nz + 16 * C::R) / (32 * C::R));
+  }
   if (chunks <= 0) {
     // pick the z-chunk count minimising waves x (planes + pipeline fill) per CTA
     int dev = 0, sms = 148, per = 1;
@@ -437,6 +511,9 @@ int launchStarT(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
   P.chunk = (P.nz + chunks - 1) / chunks;
   P.nchunks = (P.nz + P.chunk - 1) / P.chunk;
   P.boundary_last = L.zorder_boundary_last;
+  P.flags = L.wait_flags;
+  P.epoch = L.wait_epoch;
+  P.wmask = L.wait_mask;
   P.out = static_cast<T *>(L.out);
   P.w0 = fromBits<T>(s.w0);
   for (int t = 0; t < 3; ++t) {
@@ -446,11 +523,42 @@ int launchStarT(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
   }
   P.scale = fromBits<T>(s.scale);
   P.two = fromBits<T>(s.two);
-  const unsigned blocks = unsigned(ntiles) * unsigned(P.nchunks);
+  P.cy = 1;
+  if (RANK == 3) {
+    P.cy = HG_CLUSTER_Y;
+    if (const char *e = std::getenv("HG_CLUSTER")) // tuning experiments only
+      P.cy = std::max(1, std::atoi(e));
+    P.cy = std::min(P.cy, P.tiles_y);
+  }
+  P.bands = (P.tiles_y + P.cy - 1) / P.cy;
+  P.order = HG_ORDER;
+  if (const char *e = std::getenv("HG_ORDER")) // tuning experiments only
+    P.order = std::atoi(e);
+  if (P.cy > 1)
+    P.order = 0;
+  unsigned blocks = unsigned(P.cy) * P.tiles_x * P.bands * P.nchunks;
+  if (P.order == 2)
+    blocks = unsigned((P.tiles_x + 3) / 4) * ((P.tiles_y + 3) / 4) * 16 * P.nchunks;
   if (blocks_out)
     *blocks_out = int(blocks);
-  kern<<<blocks, C::NTHREADS, C::SMEM, st>>>(*L.tm_cur, *L.tm_prev, P);
-  return cudaErr(cudaGetLastError(), "star kernel launch");
+  if (P.cy == 1) {
+    kern<<<blocks, C::NTHREADS, C::SMEM, st>>>(*L.tm_cur, *L.tm_prev, P);
+    return cudaErr(cudaGetLastError(), "star kernel launch");
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(C::NTHREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(P.cy);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaErr(cudaLaunchKernelEx(&cfg, kern, *L.tm_cur, *L.tm_prev, P),
+                 "star kernel cluster launch");
 }
 
 template <typename T, int RANK, int NT, int KIND> int residentT() {
@@ -644,6 +752,26 @@ template <typename T> __global__ void putKernel(const __grid_constant__ PutParam
   const int64_t w = P.L.rank == 3 ? J.size[2] : (P.L.rank == 2 ? J.size[1] : J.size[0]);
   const T *src = static_cast<const T *>(J.src);
   T *dst = static_cast<T *>(J.dst);
+  // 16-byte path when both rows start 16-byte aligned (z/y faces: rows of the core width,
+  // starting at the 128-byte-aligned core column)
+  constexpr int VE = 16 / sizeof(T);
+  const int64_t lastS = P.L.rank == 3 ? J.src_at[2] : (P.L.rank == 2 ? J.src_at[1] : J.src_at[0]);
+  const int64_t lastD = P.L.rank == 3 ? J.dst_at[2] : (P.L.rank == 2 ? J.dst_at[1] : J.dst_at[0]);
+  const bool vec = P.L.rank >= 2 && w % VE == 0 && (P.L.col0 + lastS) % VE == 0 &&
+                   (P.L.col0 + lastD) % VE == 0 && P.L.pitch % VE == 0;
+  if (vec) {
+    for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
+      int64_t i0 = P.L.rank == 3 ? r / J.size[1] : r, i1 = P.L.rank == 3 ? r % J.size[1] : 0;
+      const int64_t se = P.L.rank == 3 ? boxElem(P.L, J.src_at, i0, i1, 0)
+                                       : boxElem(P.L, J.src_at, i0, 0, 0);
+      const int64_t de = P.L.rank == 3 ? boxElem(P.L, J.dst_at, i0, i1, 0)
+                                       : boxElem(P.L, J.dst_at, i0, 0, 0);
+      const int4 *s4 = reinterpret_cast<const int4 *>(src + se);
+      int4 *d4 = reinterpret_cast<int4 *>(dst + de);
+      for (int64_t c = threadIdx.x; c < w / VE; c += blockDim.x)
+        d4[c] = s4[c];
+    }
+  } else
   for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
     int64_t i0, i1;
     if (P.L.rank == 3) {
@@ -740,15 +868,19 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
   const CUtensorMapDataType dt =
       dtype == HG_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   cuuint32_t boxCur[3] = {cuuint32_t(TX + 8), cuuint32_t(TY + 2 * RY), 1};
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char *e = std::getenv("HG_L2PROMO")) // tuning experiments only
+    promo = e[0] == '0' ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+            : e[0] == '1' ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+            : e[0] == '2' ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                          : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
   CUresult r = encode(cur, dt, 3, base, dims, strides, boxCur, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled(cur) failed: " + std::to_string(int(r)));
   cuuint32_t boxPrev[3] = {cuuint32_t(TX), cuuint32_t(TY), 1};
   r = encode(prev, dt, 3, base, dims, strides, boxPrev, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+             CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled(prev) failed: " + std::to_string(int(r)));
   return HG_OK;

@@ -35,6 +35,9 @@ struct StarLaunch {
   void *out;                  // base of the output buffer allocation
   int chunks;                 // z-chunks (0 = auto)
   int zorder_boundary_last;   // process z-boundary chunks last (dmp overlap)
+  const unsigned long long *wait_flags = nullptr; // dmp: my flag words (null = no wait)
+  unsigned long long wait_epoch = 0;
+  int wait_mask = 0;
 };
 // Creates the TMA descriptor of a buffer for the star family's cur/prev boxes.
 int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay,

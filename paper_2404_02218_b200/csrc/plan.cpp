@@ -111,6 +111,10 @@ int planStep(hg_plan &p, cudaStream_t st) {
     L.out = p.dptr[static_cast<size_t>(bOut)];
     L.chunks = p.chunks;
     L.zorder_boundary_last = p.boundaryLast;
+    L.wait_flags = p.waitFlags;
+    L.wait_epoch = p.waitEpoch;
+    L.wait_mask = p.waitMask;
+    p.waitFlags = nullptr;
     int st2 = launchStar(L, st, nullptr);
     if (st2)
       return st2;

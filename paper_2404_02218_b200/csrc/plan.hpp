@@ -23,6 +23,10 @@ struct hg_plan {
   int64_t launches = 0;
   int chunks = 0;                     // star z-chunks (0 = auto)
   int boundaryLast = 0;               // star: z-boundary chunks last (dmp overlap)
+  // one-shot (consumed by the next planStep): halo faces the star kernel must wait for
+  const unsigned long long *waitFlags = nullptr;
+  unsigned long long waitEpoch = 0;
+  int waitMask = 0;
 };
 
 namespace hg {

@@ -1,0 +1,51 @@
+"""Multi-rank plumbing: one process per GPU, torch.distributed only for the host-side
+handshake (CUDA IPC handle exchange, barriers, max-over-ranks timing).  The halo data itself
+moves GPU-to-GPU over NVLink through the dmp put kernels (hg_dmp_run)."""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+from . import coord_from_rank, neighbor_rank
+
+
+def face_neighbors(rank: int, grid: Sequence[int]) -> List[int]:
+    """Ranks one step away along each grid dimension (no wrap, dmp_ops.cpp:39-49)."""
+    out = []
+    for d in range(len(grid)):
+        for s in (-1, 1):
+            dirv = [0] * len(grid)
+            dirv[d] = s
+            n = neighbor_rank(rank, dirv, grid)
+            if n >= 0 and n not in out:
+                out.append(n)
+    return out
+
+
+def weak_grid(world: int, ndim: int = 3) -> List[int]:
+    """Slabs along dim 0: faces are contiguous planes, <= 2 neighbours per rank."""
+    return [world] + [1] * (ndim - 1)
+
+
+def strong_grid(world: int) -> List[int]:
+    """Near-cubic process grids for a fixed global domain (1, 2x1x1, 2x2x1, 2x2x2)."""
+    table = {1: [1, 1, 1], 2: [2, 1, 1], 4: [2, 2, 1], 8: [2, 2, 2]}
+    if world in table:
+        return table[world]
+    return weak_grid(world)
+
+
+def connect(dmp, rank: int, grid: Sequence[int], world: int, group=None) -> List[int]:
+    """All-gather every rank's IPC blob; import those of the face neighbours."""
+    import torch.distributed as dist
+    blobs = [None] * world
+    dist.all_gather_object(blobs, dmp.export(), group=group)
+    nbrs = face_neighbors(rank, grid)
+    for r in nbrs:
+        dmp.import_peer(r, blobs[r])
+    return nbrs
+
+
+def origin_of(rank: int, grid: Sequence[int], core: Sequence[int]) -> List[int]:
+    """Global logical offset of a rank's local buffers (scatterRank, simulator.cpp:995-1025)."""
+    c = coord_from_rank(rank, grid)
+    return [c[d] * core[d] for d in range(len(grid))]

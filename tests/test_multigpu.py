@@ -38,3 +38,25 @@ def test_ipc_dmp_two_ranks(args):
         r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
         assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec,grid,T", [
+    (("wave", 3, 24, 8), [3, 1, 1], 4), (("heat", 3, 24, 4), [2, 2, 1], 4),
+    (("heat", 2, 24, 2), [2, 2], 3),
+])
+def test_simulate_ranks_spread_over_devices(port, spec, grid, T):
+    # one process, ranks round-robin over the visible GPUs: peer pointers + cross-device events
+    import numpy as np
+    import paper_2404_02218_b200 as hg
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    init = hg.initial_fields(prog)
+    nr = int(np.prod(grid))
+    out = hg.simulate(prog, grid, init, T, devices=[r % n for r in range(nr)])
+    arrays = [b.data.copy() for b in init]
+    perm = port.run(prog, arrays, T)
+    for b, p in zip(out, perm):
+        assert np.array_equal(b.data.view(np.uint32), arrays[p].view(np.uint32))

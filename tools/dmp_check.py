@@ -37,11 +37,8 @@ def main():
     coord = hg.coord_from_rank(rank, grid)
     plan.init_fields(origin=[coord[d] * dc.core[d] for d in range(a.rank)])
     dmp = hg.Dmp(plan, dc, rank)
-    blobs = [None] * world
-    dist.all_gather_object(blobs, dmp.export())
-    for r, b in enumerate(blobs):
-        if r != rank:
-            dmp.import_peer(r, b)
+    from paper_2404_02218_b200 import dist as hd
+    hd.connect(dmp, rank, grid, world)
     dist.barrier()
     dmp.run(a.T)
     torch.cuda.synchronize()
