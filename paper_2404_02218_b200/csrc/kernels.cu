@@ -33,6 +33,9 @@
 #ifndef HG_ORDER
 #define HG_ORDER 0
 #endif
+#ifndef HG_MINB_R4
+#define HG_MINB_R4 1
+#endif
 
 namespace hg {
 
@@ -202,7 +205,7 @@ template <typename T, int RANK, int NT, int KIND> struct StarCfg {
   static constexpr int NWARPS_C = NCONS / 32;
   static constexpr int NTHREADS = NCONS + 32;
   // CTAs per SM the register budget must allow (f32 3D: 3 for r<=2, 2 for r=4)
-  static constexpr int MINB = RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? 3 : 2) : 1) : 4;
+  static constexpr int MINB = RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? 3 : HG_MINB_R4) : 1) : 4;
   static constexpr int DEPTH = RANK == 3 ? (R <= 2 ? HG_DEPTH3 : HG_DEPTH3W) : HG_DEPTH2;
   static constexpr int NS = R + 1 + DEPTH;
   static constexpr int Q = 2 * R + 1;
