@@ -13,6 +13,8 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 
@@ -43,6 +45,8 @@ struct hg_dmp {
   bool opened[kDirs] = {};
   unsigned long long *flags = nullptr; // my flag words, one per incoming direction
   unsigned int *counter = nullptr;
+  unsigned int *cnt6 = nullptr;        // per-face CTA completion counters of fused swaps
+  unsigned int cntAccum[kDirs] = {};   // their cumulative targets (host mirror)
   unsigned long long epoch = 0;
   std::vector<char> dirty;             // per buffer: written since its last swap
   int64_t bytes = 0;
@@ -186,6 +190,10 @@ int hg_dmp_create(hg_plan *plan, const hg_decomp *dc, int64_t rank, hg_dmp **out
     if (st)
       return st;
     cudaMemset(d->counter, 0, 64);
+    st = cudaCheck(cudaMalloc(&d->cnt6, 64), "cudaMalloc(cnt6)");
+    if (st)
+      return st;
+    cudaMemset(d->cnt6, 0, 64);
     st = cudaCheck(cudaEventCreateWithFlags(&d->putDone, cudaEventDisableTiming), "event");
     if (st)
       return st;
@@ -214,6 +222,7 @@ int hg_dmp_destroy(hg_dmp *d) {
       }
   cudaFree(d->flags);
   cudaFree(d->counter);
+  cudaFree(d->cnt6);
   if (d->putDone)
     cudaEventDestroy(d->putDone);
   delete d;
@@ -292,40 +301,53 @@ int hg_dmp_run(hg_dmp *d, int64_t steps, void *stream) {
       return setError(HG_ESTATE, "neighbour rank " + std::to_string(d->nbr[di]) +
                                      " has not been imported");
   hg_plan &p = *d->plan;
+  const hg_program &g = p.prog;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = cudaCheck(cudaSetDevice(p.device), "cudaSetDevice");
   if (rc)
     return rc;
+  PutSignal sig[kDirs];
+  int nsig = 0, widx[kDirs], nw = 0, mask = 0;
+  for (int di = 0; di < kDirs; ++di) {
+    if (d->nbr[di] < 0)
+      continue;
+    sig[nsig++].flag = d->peerFlags[di] + (di ^ 1); // the neighbour receives on its opposite
+    widx[nw++] = di;
+    mask |= 1 << di;
+  }
+  const bool star = p.an.family == Family::Star && g.nresults == 1;
   std::vector<PutJob> jobs;
+  // HG_DMP_PROFILE=1: event timing of the put and stencil phases (diagnostics only)
+  static const bool prof = std::getenv("HG_DMP_PROFILE") != nullptr;
+  std::vector<cudaEvent_t> evs;
+  auto mark = [&]() {
+    if (!prof)
+      return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    evs.push_back(e);
+  };
+  bool roundReady = false; // the previous step's kernel already published this step's round
   for (int64_t t = 0; t < steps; ++t) {
+    // 1. standalone put of every dirty swapped buffer (first step of a call, or whatever the
+    //    fused path did not cover)
     jobs.clear();
     rc = buildJobs(*d, jobs);
     if (rc)
       return rc;
-    ++d->epoch;
-    PutSignal sig[kDirs];
-    int nsig = 0, widx[kDirs], nw = 0;
-    for (int di = 0; di < kDirs; ++di) {
-      if (d->nbr[di] < 0)
-        continue;
-      // the neighbour at my direction di receives on its opposite direction
-      const int opp = di ^ 1;
-      sig[nsig++].flag = d->peerFlags[di] + opp;
-      widx[nw++] = di;
+    mark();
+    if (!roundReady || !jobs.empty()) {
+      ++d->epoch;
+      rc = launchPut(jobs.data(), static_cast<int>(jobs.size()), devLayout(p.lay[0]), sig, nsig,
+                     d->epoch, d->counter, st);
+      if (rc)
+        return rc;
+      if (nsig || !jobs.empty())
+        ++p.launches;
     }
-    rc = launchPut(jobs.data(), static_cast<int>(jobs.size()), devLayout(p.lay[0]), sig, nsig,
-                   d->epoch, d->counter, st);
-    if (rc)
-      return rc;
-    if (nsig || !jobs.empty())
-      ++p.launches;
-    if (p.an.family == Family::Star && nw) {
-      // fused wait: only the CTAs whose halo rows touch a neighbour's face wait for its
-      // flag, inside the stencil kernel; z-boundary chunks run last, so the exchange
-      // overlaps the interior
-      int mask = 0;
-      for (int k = 0; k < nw; ++k)
-        mask |= 1 << widx[k];
+    // 2. the stencil step; halo-reading CTAs wait for the round in-kernel
+    if (star && nw) {
       p.waitFlags = d->flags;
       p.waitEpoch = d->epoch;
       p.waitMask = mask;
@@ -337,16 +359,109 @@ int hg_dmp_run(hg_dmp *d, int64_t steps, void *stream) {
       if (nw)
         ++p.launches;
     }
+    // 3. fuse the NEXT step's swap of the output into this kernel (not on the last step of
+    //    the call: the reference swaps a buffer only right before it is loaded)
+    const int bOut = p.bind[static_cast<size_t>(g.store_field[0])];
+    int nextSlot = -1; // the argument slot the output buffer occupies next step
+    for (size_t i = 0; i < p.an.src.size(); ++i)
+      if (p.an.src[i] == g.store_field[0])
+        nextSlot = static_cast<int>(i);
+    const hg_swap *sw = nullptr;
+    for (int k = 0; k < d->dc.nswaps && nextSlot >= 0; ++k)
+      if (d->dc.swaps[k].field == nextSlot)
+        sw = &d->dc.swaps[k];
+    bool fused = false;
+    static const bool noFuse = std::getenv("HG_NOFUSE") != nullptr; // A/B experiments only
+    if (star && nw && sw && t + 1 < steps && !noFuse) {
+      StarLaunch &F = p.fuse;
+      F = StarLaunch{};
+      const Layout &L = p.lay[static_cast<size_t>(bOut)];
+      const int r = g.rank;
+      int64_t stride[3] = {0, 0, 1};
+      if (r == 3) {
+        stride[0] = L.pitch * L.shape[1];
+        stride[1] = L.pitch;
+      } else {
+        stride[0] = L.pitch;
+      }
+      // kernel face index: 2*kdim + (sign>0) with kdim 0 = z (dim 0), 1 = y, RANK-1 = x
+      for (int k = 0; k < sw->nexchanges; ++k) {
+        const hg_exchange &e = sw->ex[k];
+        int dim = -1, sign = 0;
+        for (int q = 0; q < r; ++q)
+          if (e.to[q] != 0) {
+            dim = q;
+            sign = e.to[q] > 0 ? 1 : -1;
+          }
+        const int di = dirIndex(dim, sign);
+        if (dim < 0 || d->nbr[di] < 0)
+          continue;
+        const hg_exchange *m = mateOf(*sw, e, r);
+        if (!m || !d->peer[di][bOut])
+          return setError(HG_ESTATE, "neighbour buffers are not connected");
+        int64_t delta = 0;
+        for (int q = 0; q < r; ++q)
+          delta += (m->at[q] - (e.at[q] + e.offset[q])) * (r == 3 ? stride[q] : (q == 0 ? stride[0] : 1));
+        F.hs[di] = static_cast<int>(e.size[dim]);
+        F.peer[di] = d->peer[di][bOut];
+        static const bool scratch = std::getenv("HG_FUSE_SCRATCH") != nullptr; // A/B only
+        if (scratch) {
+          static void *buf = nullptr;
+          if (!buf)
+            cudaMalloc(&buf, L.bytes());
+          F.peer[di] = buf;
+        }
+        F.pdelta[di] = delta;
+        F.peer_flag[di] = d->peerFlags[di];
+        d->bytes += [&] {
+          int64_t n = 1;
+          for (int q = 0; q < r; ++q)
+            n *= e.size[q];
+          return n * L.es;
+        }();
+      }
+      F.fuse = 1;
+      F.cnt = d->cnt6;
+      F.cnt_accum = d->cntAccum;
+      F.put_epoch = d->epoch + 1;
+      fused = true;
+    }
+    mark();
     rc = planStep(p, st);
     if (rc)
       return rc;
-    // the step's outputs (bound before rotation) are now dirty
-    const hg_program &g = p.prog;
-    std::vector<int> prevBind(p.bind.size());
-    for (size_t i = 0; i < p.bind.size(); ++i)
-      prevBind[static_cast<size_t>(p.an.src[i])] = p.bind[i];
-    for (int k = 0; k < g.nresults; ++k)
+    mark();
+    d->dirty[static_cast<size_t>(bOut)] = fused ? 0 : 1;
+    for (int k = 1; k < g.nresults; ++k) { // (multi-result programs never fuse)
+      std::vector<int> prevBind(p.bind.size());
+      for (size_t i = 0; i < p.bind.size(); ++i)
+        prevBind[static_cast<size_t>(p.an.src[i])] = p.bind[i];
       d->dirty[static_cast<size_t>(prevBind[static_cast<size_t>(g.store_field[k])])] = 1;
+    }
+    if (fused)
+      ++d->epoch;
+    roundReady = fused;
+  }
+  if (prof && !evs.empty()) {
+    cudaStreamSynchronize(st);
+    double put = 0, ker = 0, gap = 0;
+    float ms;
+    const size_t n = evs.size() / 3;
+    for (size_t i = 0; i < n; ++i) {
+      cudaEventElapsedTime(&ms, evs[3 * i], evs[3 * i + 1]);
+      put += ms;
+      cudaEventElapsedTime(&ms, evs[3 * i + 1], evs[3 * i + 2]);
+      ker += ms;
+      if (i + 1 < n) {
+        cudaEventElapsedTime(&ms, evs[3 * i + 2], evs[3 * i + 3]);
+        gap += ms;
+      }
+    }
+    std::fprintf(stderr, "[hg_dmp rank %lld] steps %zu: put %.1f us, stencil %.1f us, gap %.1f us (avg)\n",
+                 static_cast<long long>(d->rank), n, 1e3 * put / n, 1e3 * ker / n,
+                 n > 1 ? 1e3 * gap / (n - 1) : 0.0);
+    for (auto e : evs)
+      cudaEventDestroy(e);
   }
   return HG_OK;
 }

@@ -36,6 +36,9 @@
 #ifndef HG_MINB_R4
 #define HG_MINB_R4 1
 #endif
+#ifndef HG_TYT_R4
+#define HG_TYT_R4 16
+#endif
 
 namespace hg {
 
@@ -152,11 +155,13 @@ __device__ __forceinline__ void st4(double *p, const V4<double> &v) {
 // Consumer threads own 4 consecutive x points each; the centre values of the 2R+1 planes
 // around the output plane live in registers (the z queue), x/y neighbours are read from the
 // staged plane with 16-byte LDS.  Output planes are stored straight to HBM (STG.128).
-template <int RANK> struct StarGeom;
-template <> struct StarGeom<3> {
-  static constexpr int TXT = 16, TYT = 16;
+// Column-tile geometry: TXT x TYT consumer threads, 4 x-points each.  3D radius-4 tiles are
+// taller (more consumer warps in the single CTA an SM holds at ~110 registers).
+template <int RANK, int R> struct StarGeom;
+template <int R> struct StarGeom<3, R> {
+  static constexpr int TXT = 16, TYT = R >= 4 ? HG_TYT_R4 : 16;
 };
-template <> struct StarGeom<2> {
+template <int R> struct StarGeom<2, R> {
   static constexpr int TXT = 32, TYT = 1;
 };
 
@@ -174,6 +179,17 @@ template <typename T> struct StarParams {
   const unsigned long long *flags;
   unsigned long long epoch;
   int wmask;     // bit 2*dim + (sign > 0): a neighbour sends into that face
+  // fused swap of the NEXT step: output points inside a send box (width hs[d] at face d) are
+  // also stored into the neighbour's buffer (peer[d] + my index + pdelta[d]); each face's
+  // CTAs count completions and the last one publishes put_epoch to the neighbour's flag
+  int fuse;
+  int hs[6];
+  T *peer[6];
+  int64_t pdelta[6];
+  unsigned int *cnt;
+  unsigned int cnt_target[6];
+  unsigned long long *peer_flag[6];
+  unsigned long long put_epoch;
   int boundary_last;
   T *out;
   T w0, wz[3], wy[3], wx[3], scale, two;
@@ -196,7 +212,7 @@ template <> struct Taps<3> {
 template <typename T, int RANK, int NT, int KIND> struct StarCfg {
   static constexpr int R = Taps<NT>::R;
   static constexpr int RY = RANK == 3 ? R : 0;
-  static constexpr int TXT = StarGeom<RANK>::TXT, TYT = StarGeom<RANK>::TYT;
+  static constexpr int TXT = StarGeom<RANK, R>::TXT, TYT = StarGeom<RANK, R>::TYT;
   static constexpr int TX = TXT * 4, TY = TYT;
   static constexpr int PADX = 4;
   static constexpr int CW = TX + 2 * PADX;
@@ -357,6 +373,21 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND>::NTHREADS,
                        (RANK == 3 ? int64_t(P.ys + yb + ty) * P.pitch : 0) + P.col0 + P.xs +
                        xb + x0);
   const int xrem = P.nx - (xb + x0);
+  // fused-swap geometry: faces this thread's row feeds (y) and x faces of its 4 points
+  int blockTouch = 0;
+  if (P.fuse) {
+    constexpr int XD = RANK - 1;
+    // CTA-uniform: which send boxes does this CTA's output region intersect?
+    if (P.hs[0] && zb < P.hs[0]) blockTouch |= 1;
+    if (P.hs[1] && zb + n > P.nz - P.hs[1]) blockTouch |= 2;
+    if (RANK == 3) {
+      if (P.hs[2] && yb < P.hs[2]) blockTouch |= 4;
+      if (P.hs[3] && min(yb + C::TY, P.ny) > P.ny - P.hs[3]) blockTouch |= 8;
+    }
+    if (P.hs[2 * XD] && xb < P.hs[2 * XD]) blockTouch |= 1 << (2 * XD);
+    if (P.hs[2 * XD + 1] && min(xb + C::TX, P.nx) > P.nx - P.hs[2 * XD + 1])
+      blockTouch |= 2 << (2 * XD);
+  }
 
   int sN = (2 * R) % NS, phN = ((2 * R) / NS) & 1; // stage/parity of the plane arriving
   int sC = R % NS;                                  // stage of the plane being computed
@@ -445,10 +476,75 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND>::NTHREADS,
 
   for (int mb = 0; mb < n; mb += Q)
     unrolled(plane, mb, std::make_integer_sequence<int, Q>{});
+
+  if (P.fuse && blockTouch) {
+    // Fused swap of the next step: the send-box points this thread produced (re-read from its
+    // own stores, L1/L2-hot) go straight into the neighbours' halos over NVLink.  Done after
+    // the plane loop so the streaming loop carries no extra registers.
+    if (yok) {
+      constexpr int XD = RANK - 1;
+      const T *src = outRow;
+      const int64_t e0 = outRow - P.out;
+      for (int d = 0; d < 2 * RANK; ++d) {
+        if (!(blockTouch & (1 << d)))
+          continue;
+        const int dim = d >> 1;
+        const bool lo = (d & 1) == 0;
+        int m0 = 0, m1 = n; // planes of this chunk inside the send box
+        if (dim == 0) {
+          if (lo) {
+            m1 = min(n, P.hs[d] - zb);
+          } else {
+            m0 = max(0, P.nz - P.hs[d] - zb);
+          }
+        } else if (RANK == 3 && dim == 1) {
+          const int yo = yb + ty;
+          if (lo ? yo >= P.hs[d] : yo < P.ny - P.hs[d])
+            continue;
+        }
+        int jmask = 0xF; // x points of this thread inside the box
+        if (dim == XD) {
+          jmask = 0;
+          for (int j = 0; j < 4; ++j) {
+            const int xo = xb + x0 + j;
+            if (lo ? xo < P.hs[d] : xo >= P.nx - P.hs[d])
+              jmask |= 1 << j;
+          }
+          if (!jmask)
+            continue;
+        }
+        T *dst = P.peer[d] + e0 + P.pdelta[d];
+        for (int m = m0; m < m1; ++m) {
+          const int64_t off = int64_t(m) * P.plane;
+          if (jmask == 0xF && xrem >= 4) {
+            st4(dst + off, ld4(src + off));
+          } else {
+            for (int j = 0; j < 4; ++j)
+              if ((jmask >> j & 1) && j < xrem)
+                dst[off + j] = src[off + j];
+          }
+        }
+      }
+    }
+    // publish: every face this CTA fed is counted; the last CTA of a face releases the epoch
+    __threadfence_system();
+    asm volatile("bar.sync 1, %0;" ::"r"(C::NCONS) : "memory");
+    if (tid == 0)
+      for (int d = 0; d < 6; ++d)
+        if (blockTouch & (1 << d)) {
+          const unsigned int old = atomicAdd(P.cnt + d, 1u);
+          if (old + 1 == P.cnt_target[d]) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.peer_flag[d] + (d ^ 1)),
+                         "l"(P.put_epoch)
+                         : "memory");
+          }
+        }
+  }
 }
 
 template <typename T, int RANK, int NT, int KIND>
-int launchStarT(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
+int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   using C = StarCfg<T, RANK, NT, KIND>;
   auto kern = starKernel<T, RANK, NT, KIND>;
   // function attributes are per device: opt in to the large shared-memory carve-out on
@@ -517,6 +613,41 @@ int launchStarT(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
   P.flags = L.wait_flags;
   P.epoch = L.wait_epoch;
   P.wmask = L.wait_mask;
+  P.fuse = L.fuse;
+  if (L.fuse) {
+    // CTAs whose output region meets each face's send box (the kernel's blockTouch)
+    auto touching = [](int ext, int tile, int ntl, int h, bool lo) {
+      int c = 0;
+      for (int i = 0; i < ntl; ++i) {
+        const int b = i * tile, e = std::min(b + tile, ext);
+        if (lo ? b < h : e > ext - h)
+          ++c;
+      }
+      return c;
+    };
+    const int nyt = RANK == 3 ? P.tiles_y : 1;
+    for (int d = 0; d < 6; ++d) {
+      P.hs[d] = L.hs[d];
+      P.peer[d] = static_cast<T *>(L.peer[d]);
+      P.pdelta[d] = L.pdelta[d];
+      P.peer_flag[d] = L.peer_flag[d];
+      if (!L.hs[d])
+        continue;
+      const int dim = d / 2;
+      const bool lo = (d & 1) == 0;
+      long c;
+      if (dim == 0)
+        c = long(touching(P.nz, P.chunk, P.nchunks, L.hs[d], lo)) * P.tiles_x * nyt;
+      else if (RANK == 3 && dim == 1)
+        c = long(touching(P.ny, C::TY, P.tiles_y, L.hs[d], lo)) * P.tiles_x * P.nchunks;
+      else
+        c = long(touching(P.nx, C::TX, P.tiles_x, L.hs[d], lo)) * nyt * P.nchunks;
+      L.cnt_accum[d] += unsigned(c);
+      P.cnt_target[d] = L.cnt_accum[d];
+    }
+    P.cnt = L.cnt;
+    P.put_epoch = L.put_epoch;
+  }
   P.out = static_cast<T *>(L.out);
   P.w0 = fromBits<T>(s.w0);
   for (int t = 0; t < 3; ++t) {
@@ -573,7 +704,7 @@ template <typename T, int RANK, int NT, int KIND> int residentT() {
   return per;
 }
 
-template <typename T, int RANK> int dispatchNT(const StarLaunch &L, cudaStream_t st, int *b) {
+template <typename T, int RANK> int dispatchNT(StarLaunch &L, cudaStream_t st, int *b) {
   const StarSpec &s = *L.spec;
   if (s.kind == kHeat) {
     if (s.ntaps == 1) return launchStarT<T, RANK, 1, kHeat>(L, st, b);
@@ -851,8 +982,8 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = dtype == HG_F32 ? 4 : 8;
   const int R = s.radius;
-  const int TX = (rank == 3 ? StarGeom<3>::TXT : StarGeom<2>::TXT) * 4;
-  const int TY = rank == 3 ? StarGeom<3>::TYT : 1;
+  const int TX = (rank == 3 ? StarGeom<3, 1>::TXT : StarGeom<2, 1>::TXT) * 4;
+  const int TY = rank == 3 ? (R >= 4 ? StarGeom<3, 4>::TYT : StarGeom<3, 1>::TYT) : 1;
   const int RY = rank == 3 ? R : 0;
   cuuint64_t dims[3], strides[2];
   dims[0] = cuuint64_t(lay.pitch);
@@ -889,7 +1020,7 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
   return HG_OK;
 }
 
-int launchStar(const StarLaunch &L, cudaStream_t st, int *blocks_out) {
+int launchStar(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   if (L.dtype == HG_F32)
     return L.rank == 3 ? dispatchNT<float, 3>(L, st, blocks_out)
                        : dispatchNT<float, 2>(L, st, blocks_out);

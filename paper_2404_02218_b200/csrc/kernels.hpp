@@ -38,11 +38,20 @@ struct StarLaunch {
   const unsigned long long *wait_flags = nullptr; // dmp: my flag words (null = no wait)
   unsigned long long wait_epoch = 0;
   int wait_mask = 0;
+  // fused swap of the next step (see StarParams in kernels.cu); cnt_accum is host state
+  int fuse = 0;
+  int hs[6] = {0, 0, 0, 0, 0, 0};
+  void *peer[6] = {};
+  int64_t pdelta[6] = {0, 0, 0, 0, 0, 0};
+  unsigned int *cnt = nullptr;
+  unsigned int *cnt_accum = nullptr;
+  unsigned long long *peer_flag[6] = {};
+  unsigned long long put_epoch = 0;
 };
 // Creates the TMA descriptor of a buffer for the star family's cur/prev boxes.
 int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay,
                        void *base, CUtensorMap *cur, CUtensorMap *prev);
-int launchStar(const StarLaunch &L, cudaStream_t st, int *blocks_out);
+int launchStar(StarLaunch &L, cudaStream_t st, int *blocks_out);
 int starResidentBlocks(const StarSpec &s, int dtype, int rank);
 
 // ---- generic bytecode kernel ------------------------------------------------------------

@@ -115,6 +115,19 @@ int planStep(hg_plan &p, cudaStream_t st) {
     L.wait_epoch = p.waitEpoch;
     L.wait_mask = p.waitMask;
     p.waitFlags = nullptr;
+    if (p.fuse.fuse) {
+      L.fuse = 1;
+      for (int d = 0; d < 6; ++d) {
+        L.hs[d] = p.fuse.hs[d];
+        L.peer[d] = p.fuse.peer[d];
+        L.pdelta[d] = p.fuse.pdelta[d];
+        L.peer_flag[d] = p.fuse.peer_flag[d];
+      }
+      L.cnt = p.fuse.cnt;
+      L.cnt_accum = p.fuse.cnt_accum;
+      L.put_epoch = p.fuse.put_epoch;
+      p.fuse.fuse = 0;
+    }
     int st2 = launchStar(L, st, nullptr);
     if (st2)
       return st2;

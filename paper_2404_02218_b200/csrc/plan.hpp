@@ -27,6 +27,7 @@ struct hg_plan {
   const unsigned long long *waitFlags = nullptr;
   unsigned long long waitEpoch = 0;
   int waitMask = 0;
+  hg::StarLaunch fuse{};              // one-shot: fused-swap fields (fuse.fuse != 0)
 };
 
 namespace hg {

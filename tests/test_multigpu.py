@@ -23,12 +23,18 @@ def _ngpus():
     ["--kind", "heat", "--rank", "3", "--extent", "48", "--order", "4", "--T", "6"],
     ["--kind", "wave", "--rank", "3", "--extent", "40", "--order", "8", "--T", "5"],
     ["--kind", "heat", "--rank", "2", "--extent", "64", "--order", "2", "--T", "7"],
+    ["--kind", "wave", "--rank", "3", "--extent", "64", "--order", "4", "--T", "9",
+     "--calls", "1,3,5"],
+    ["--kind", "heat", "--rank", "3", "--extent", "100", "--order", "8", "--T", "6",
+     "--calls", "4,2"],
 ])
 def test_ipc_dmp_two_ranks(args):
     n = _ngpus()
     if n < 2:
         pytest.skip("needs 2 GPUs")
-    for nproc, grid in ((2, None), (min(n, 4), "2x2x1" if "3" == args[3] else "2x2")):
+    for nproc, grid in ((2, None), (min(n, 4), "2x2x1" if "3" == args[3] else "2x2"),
+                        (min(n, 4), "1x2x2" if "3" == args[3] else "1x4"),
+                        (min(n, 4), "4x1x1" if "3" == args[3] else "4x1")):
         if nproc < 4 and grid:
             continue
         cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone",

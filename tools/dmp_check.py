@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--order", type=int, default=4)
     ap.add_argument("--grid", default=None)
     ap.add_argument("--T", type=int, default=5)
+    ap.add_argument("--calls", default=None, help="split T over several run calls, e.g. 2,3")
     a = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -40,7 +41,10 @@ def main():
     from paper_2404_02218_b200 import dist as hd
     hd.connect(dmp, rank, grid, world)
     dist.barrier()
-    dmp.run(a.T)
+    calls = [int(x) for x in a.calls.split(",")] if a.calls else [a.T]
+    assert sum(calls) == a.T
+    for c in calls:
+        dmp.run(c)
     torch.cuda.synchronize()
     perm, _ = plan.binding()
     got = [plan.download(p) for p in perm]

@@ -1,0 +1,3 @@
+HG_ONLY=wave3d_so8_1024,heat3d_so4_1024,heat3d_so4_512 HG_CHUNKS=0 timeout 600 python tools/sweep.py 2>&1 | grep -v JSON
+HG_DMP_PROFILE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 2 --steps 200 --warmup 5 --no-e2e > gpurun_out/b2q.log 2>&1; echo "$(grep -o '"ms_per_step": [0-9.]*' gpurun_out/b2q.log)"; grep "steps 200" gpurun_out/b2q.log
+timeout 900 python -m pytest tests/test_multigpu.py -q -x 2>&1 | tail -2

@@ -1,0 +1,4 @@
+for F in 0 1; do
+if [ $F = 1 ]; then export HG_NOFUSE=1; else unset HG_NOFUSE; fi
+HG_DMP_PROFILE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 2953$F bench.py --gpus 2 --steps 200 --warmup 5 --no-e2e > gpurun_out/b2p_$F.log 2>&1; echo "n2 nofuse=$F $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/b2p_$F.log)"; grep "hg_dmp rank" gpurun_out/b2p_$F.log
+done
