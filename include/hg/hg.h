@@ -177,6 +177,11 @@ int hg_build_kernel_program(const char *kind, int rank, int64_t extent, int orde
  * ("star3d_r2_heat", "generic", ...) into name[cap]. No GPU needed. */
 int hg_program_match(const hg_program *prog, char *name, size_t cap);
 
+/* The fused-apply family (generated straight-line code for any apply DAG): generate the
+ * kernel source for `prog` and compile it with NVRTC for sm_100a, without a GPU.  Writes the
+ * generated CUDA source into src[cap] (may be NULL) and the cubin size into *cubin_bytes. */
+int hg_apply_compile(const hg_program *prog, char *src, size_t cap, size_t *cubin_bytes);
+
 /* The decompose pass on a program (dmp_transforms.cpp:101-312): rewrites *local (field bounds
  * = rank-0 core widened by the halos, stores = rank-0 core) and fills *decomp (one swap per
  * apply operand load, template exchanges).  `local` may alias `global`. */

@@ -139,6 +139,51 @@ class Program:
         self.prog.ops = C.cast(self.ops, C.POINTER(HgOp))
 
     @staticmethod
+    def from_json(j) -> "Program":
+        """A program descriptor serialised by tests/golden/make_golden.py (prog_json)."""
+        p = HgProgram()
+        ops = (HgOp * max(len(j["ops"]), 1))()
+        r = j["rank"]
+        p.rank, p.dtype, p.nfields = r, j["dtype"], j["nfields"]
+        for i, (lb, ub) in enumerate(j["fields"]):
+            for d in range(r):
+                p.fields[i].lb[d], p.fields[i].ub[d] = lb[d], ub[d]
+        p.noperands = len(j["operand_field"])
+        for i, f in enumerate(j["operand_field"]):
+            p.operand_field[i] = f
+        for i, (code, a, b, operand, off, bits) in enumerate(j["ops"]):
+            ops[i].code, ops[i].a, ops[i].b, ops[i].operand = code, a, b, operand
+            for d in range(r):
+                ops[i].off[d] = off[d]
+            ops[i].bits = int(bits, 16)
+        p.nops = len(j["ops"])
+        p.nresults = len(j["result_op"])
+        for k in range(p.nresults):
+            p.result_op[k], p.store_field[k] = j["result_op"][k], j["store_field"][k]
+            lb, ub = j["store"][k]
+            for d in range(r):
+                p.store[k].lb[d], p.store[k].ub[d] = lb[d], ub[d]
+        p.ngroups = len(j["groups"])
+        at = 0
+        for g, grp in enumerate(j["groups"]):
+            p.group_len[g] = len(grp)
+            for x in grp:
+                p.groups[at] = x
+                at += 1
+        return Program(p, ops)
+
+    @staticmethod
+    def pw_advection(nz: int, ny: int, nx: int) -> "Program":
+        """BASELINE config 4: the authored PW-advection program (programs/pw_advection.py),
+        as exported by the reference's parser, resized to nz x ny x nx."""
+        import json
+        import os
+        here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "programs",
+                            "pw_advection.json")
+        with open(here) as f:
+            return Program.from_json(json.load(f)["program"]).with_extents([nz, ny, nx])
+
+    @staticmethod
     def build(spec: KernelSpec) -> "Program":
         ops = (HgOp * capi.HG_MAX_OPS)()
         prog = HgProgram()

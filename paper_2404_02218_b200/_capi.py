@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
         "hg_build_kernel_program": (C.c_int, [C.c_char_p, C.c_int, I64, C.c_int, C.c_int,
                                               P(HgProgram), P(HgOp), C.c_int]),
         "hg_program_match": (C.c_int, [P(HgProgram), C.c_char_p, SZ]),
+        "hg_apply_compile": (C.c_int, [P(HgProgram), C.c_char_p, SZ, P(SZ)]),
         "hg_decompose_program": (C.c_int, [P(HgProgram), C.c_int, P(I64), P(HgProgram),
                                            P(HgDecomp)]),
         "hg_plan_create": (C.c_int, [P(HgProgram), C.c_int, P(V)]),

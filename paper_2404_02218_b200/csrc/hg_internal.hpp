@@ -14,7 +14,7 @@ namespace hg {
 int setError(int status, const std::string &msg);
 
 // ---- program analysis (program.cpp) ----------------------------------------------------
-enum class Family { Generic = 0, Star = 1 };
+enum class Family { Generic = 0, Star = 1, Apply = 2 };
 enum StarKind { kHeat = 0, kWave = 1, kCopy = 2 };
 
 // The star-Laplacian family the generator emits (kernels.cpp:110-135, 205-226):

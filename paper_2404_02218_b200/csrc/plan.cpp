@@ -4,7 +4,10 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <exception>
+#include <map>
+#include <mutex>
 
 namespace hg {
 
@@ -15,6 +18,24 @@ int cudaCheck(cudaError_t e, const char *what) {
 }
 
 namespace {
+
+// Generated kernels are cached per (source, device): NVRTC runs once per distinct program.
+std::shared_ptr<JitKernel> jitCached(const hg_program &g, int device) {
+  static std::mutex mu;
+  static std::map<std::pair<std::string, int>, std::shared_ptr<JitKernel>> cache;
+  auto k = std::make_shared<JitKernel>();
+  if (jitBuildSource(g, *k) != HG_OK)
+    return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(k->source, device);
+  auto it = cache.find(key);
+  if (it != cache.end())
+    return it->second;
+  if (jitCompile(*k) != HG_OK || jitLoad(*k, device) != HG_OK)
+    return nullptr;
+  cache[key] = k;
+  return k;
+}
 
 // Linear-scan slot allocation for the generic kernel: a value lives until its last use.
 int compileGeneric(hg_plan &p) {
@@ -129,6 +150,16 @@ int planStep(hg_plan &p, cudaStream_t st) {
       p.fuse.fuse = 0;
     }
     int st2 = launchStar(L, st, nullptr);
+    if (st2)
+      return st2;
+  } else if (a.family == Family::Apply) {
+    const CUtensorMap *tms[HG_MAX_FIELDS];
+    void *outs[HG_MAX_RESULTS];
+    for (int o = 0; o < g.noperands; ++o)
+      tms[o] = &p.tmApply[static_cast<size_t>(p.bind[static_cast<size_t>(g.operand_field[o])])];
+    for (int k = 0; k < g.nresults; ++k)
+      outs[k] = p.dptr[static_cast<size_t>(p.bind[static_cast<size_t>(g.store_field[k])])];
+    int st2 = jitLaunch(*p.jit, g, p.lay[0], tms, outs, p.chunks, st);
     if (st2)
       return st2;
   } else {
@@ -252,11 +283,31 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
         return st;
     }
   } else {
-    st = compileGeneric(*p);
-    if (st)
-      return st;
-    if (p->nslots > 48)
-      return setError(HG_EUNSUPPORTED, "apply region needs too many live values");
+    // any other DAG: the fused-apply family (generated straight-line code) when its tile
+    // rims cover the accesses, else the slot-interpreting generic kernel
+    std::string why;
+    if (!std::getenv("HG_NO_APPLY_JIT") && jitEligible(g, p->an, &why)) {
+      auto k = jitCached(g, device);
+      if (k) {
+        p->jit = k;
+        p->an.family = Family::Apply;
+        p->an.name = "apply" + std::to_string(g.rank) + "d_" + (g.dtype == HG_F32 ? "f32" : "f64");
+        p->tmApply.resize(static_cast<size_t>(g.nfields));
+        for (int f = 0; f < g.nfields; ++f) {
+          st = jitTensorMap(*k, g.dtype, g.rank, p->lay[static_cast<size_t>(f)],
+                            p->dptr[static_cast<size_t>(f)], &p->tmApply[static_cast<size_t>(f)]);
+          if (st)
+            return st;
+        }
+      }
+    }
+    if (p->an.family != Family::Apply) {
+      st = compileGeneric(*p);
+      if (st)
+        return st;
+      if (p->nslots > 48)
+        return setError(HG_EUNSUPPORTED, "apply region needs too many live values");
+    }
   }
   p->bind.resize(static_cast<size_t>(g.nfields));
   for (int i = 0; i < g.nfields; ++i)
@@ -281,7 +332,7 @@ int hg_plan_destroy(hg_plan *p) {
 int hg_plan_kernel_name(const hg_plan *p, char *name, size_t cap) {
   if (!p)
     return setError(HG_EINVAL, "null plan");
-  std::string n = p->an.family == Family::Star
+  std::string n = p->an.family != Family::Generic
                       ? p->an.name
                       : "generic" + std::to_string(p->prog.rank) + "d_" +
                             (p->prog.dtype == HG_F32 ? "f32" : "f64");

@@ -2,6 +2,7 @@
 #ifndef HG_PLAN_HPP
 #define HG_PLAN_HPP
 
+#include "jit.hpp"
 #include "kernels.hpp"
 
 #include <memory>
@@ -28,6 +29,8 @@ struct hg_plan {
   unsigned long long waitEpoch = 0;
   int waitMask = 0;
   hg::StarLaunch fuse{};              // one-shot: fused-swap fields (fuse.fuse != 0)
+  std::shared_ptr<hg::JitKernel> jit;  // fused-apply family (generated, per program)
+  std::vector<CUtensorMap> tmApply;   // per buffer, for the fused-apply boxes
 };
 
 namespace hg {

@@ -6,6 +6,7 @@
 
 #include <charconv>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -387,7 +388,8 @@ int analyze(const hg_program &p, Analysis &a) {
   for (int f = 1; f < p.nfields; ++f)
     if (!boundsEqual(p.fields[f], p.fields[0], p.rank))
       sameBounds = false;
-  if (p.rank >= 2 && sameBounds && Matcher(p).match(s)) {
+  // HG_NO_STAR (tests only) routes star programs through the fused-apply family
+  if (p.rank >= 2 && sameBounds && !std::getenv("HG_NO_STAR") && Matcher(p).match(s)) {
     a.family = Family::Star;
     a.star = s;
     static const char *kinds[] = {"heat", "wave", "copy"};

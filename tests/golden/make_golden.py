@@ -113,6 +113,12 @@ AUTHORED = {
 """,
 }
 
+sys.path.insert(0, REPO)
+from paper_2404_02218_b200.programs.pw_advection import xir as pw_xir  # noqa: E402
+
+AUTHORED["pw_advection_16x24x40"] = pw_xir(16, 24, 40)
+AUTHORED["pw_advection_f64_9x10x11"] = pw_xir(9, 10, 11, "f64")
+
 SERIAL = [  # (kind, rank, extent, order, f32, T)
     ("heat", 1, 16, 2, 1, 5), ("heat", 1, 128, 8, 0, 7),
     ("heat", 2, 16, 2, 1, 5), ("heat", 2, 16, 2, 0, 5), ("heat", 2, 12, 4, 1, 3),
@@ -230,6 +236,12 @@ def main():
             raise RuntimeError(ref.err())
         auth.append({"name": name, "T": T, "program": prog_json(prog, ops),
                      "init_fp": fps(ref, init), "final_fp": fps(ref, fin)})
+        if name == "pw_advection_16x24x40":  # the authored config-4 program, as data
+            with open(os.path.join(REPO, "paper_2404_02218_b200", "programs",
+                                   "pw_advection.json"), "w") as f:
+                json.dump({"generator": "reference parser + propagate-bounds on "
+                                        "programs/pw_advection.py:xir(16,24,40)",
+                           "program": prog_json(prog, ops)}, f, indent=1)
         print("authored", name, flush=True)
     out["authored"] = auth
 

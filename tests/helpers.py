@@ -8,41 +8,7 @@ from paper_2404_02218_b200 import _capi as capi
 
 
 def program_from_json(j) -> "hg.Program":
-    p = capi.HgProgram()
-    ops = (capi.HgOp * max(len(j["ops"]), 1))()
-    r = j["rank"]
-    p.rank = r
-    p.dtype = j["dtype"]
-    p.nfields = j["nfields"]
-    for i, (lb, ub) in enumerate(j["fields"]):
-        for d in range(r):
-            p.fields[i].lb[d] = lb[d]
-            p.fields[i].ub[d] = ub[d]
-    p.noperands = len(j["operand_field"])
-    for i, f in enumerate(j["operand_field"]):
-        p.operand_field[i] = f
-    for i, (code, a, b, operand, off, bits) in enumerate(j["ops"]):
-        ops[i].code, ops[i].a, ops[i].b, ops[i].operand = code, a, b, operand
-        for d in range(r):
-            ops[i].off[d] = off[d]
-        ops[i].bits = int(bits, 16)
-    p.nops = len(j["ops"])
-    p.nresults = len(j["result_op"])
-    for k in range(p.nresults):
-        p.result_op[k] = j["result_op"][k]
-        p.store_field[k] = j["store_field"][k]
-        lb, ub = j["store"][k]
-        for d in range(r):
-            p.store[k].lb[d] = lb[d]
-            p.store[k].ub[d] = ub[d]
-    p.ngroups = len(j["groups"])
-    at = 0
-    for g, grp in enumerate(j["groups"]):
-        p.group_len[g] = len(grp)
-        for x in grp:
-            p.groups[at] = x
-            at += 1
-    return hg.Program(p, ops)
+    return hg.Program.from_json(j)
 
 
 def decomp_from_json(j) -> capi.HgDecomp:

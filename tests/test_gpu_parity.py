@@ -52,13 +52,44 @@ def test_config1_full_run_bitwise(golden):
     assert [fp_hex(a) for a in fin] == ["b11e8dddf9e8c23c", "34a5556efc0dfea0"]
 
 
-def test_authored_programs_bitwise(golden):
+@pytest.mark.parametrize("family", ["apply", "generic"])
+def test_authored_programs_bitwise(golden, monkeypatch, family):
+    # multi-operand / multi-result / divide / diagonal programs incl. the authored
+    # PW-advection set: the fused-apply family (NVRTC-generated) and the generic kernel
+    if family == "generic":
+        monkeypatch.setenv("HG_NO_APPLY_JIT", "1")
     for c in golden["authored"]:
         prog = program_from_json(c["program"])
         init, fin, _, name = _plan_run(prog, c["T"])
-        assert name.startswith("generic")
+        want = family if prog.rank >= 2 else "generic"
+        assert name.startswith(want), (c["name"], name)
         assert [fp_hex(a) for a in init] == c["init_fp"], c["name"]
         assert [fp_hex(a) for a in fin] == c["final_fp"], c["name"]
+
+
+def test_pw_advection_config4_against_oracle(port):
+    # BASELINE config 4 shape: 128 x 512 x 512 (x fastest), bitwise incl. the halo rims
+    prog = hg.Program.pw_advection(128, 512, 512)
+    arrays = port.initial_fields(prog)
+    perm_o = port.run(prog, arrays, 1)
+    init, fin, perm, name = _plan_run(prog, 1)
+    assert name == "apply3d_f32" and perm == perm_o
+    for g, o in zip(fin, [arrays[p] for p in perm_o]):
+        assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
+@pytest.mark.parametrize("spec,T", [(("wave", 3, 45, 4), 4), (("heat", 3, 70, 8), 3),
+                                    (("heat", 2, 300, 2), 5)])
+def test_apply_family_on_star_programs_matches(port, monkeypatch, spec, T):
+    # the generated family also runs the generator's kernels bit-exactly
+    monkeypatch.setenv("HG_NO_STAR", "1")
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    arrays = port.initial_fields(prog)
+    perm_o = port.run(prog, arrays, T)
+    _, fin, perm, name = _plan_run(prog, T)
+    assert name.startswith("apply") and perm == perm_o
+    for g, o in zip(fin, [arrays[p] for p in perm_o]):
+        assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
 
 
 def test_run_serial_stencil_host_api(port):

@@ -127,3 +127,30 @@ def test_csv_and_throughput():
     assert hg.csv_header() == "label,core_points,steps,seconds,gpts_per_s"
     assert hg.gpts_per_sec(10**9, 2, 4.0) == 0.5
     assert hg.csv_row("x", 100, 2, 0.5).startswith("x,100,2,0.5,")
+
+
+def test_fused_apply_family_generates_and_compiles(golden):
+    # NVRTC compiles the generated straight-line kernel for sm_100a (no GPU needed)
+    import ctypes as C
+    done = 0
+    for c in golden["authored"]:
+        p = program_from_json(c["program"])
+        buf = C.create_string_buffer(1 << 20)
+        n = C.c_size_t()
+        rc = capi.lib().hg_apply_compile(C.byref(p.prog), buf, 1 << 20, C.byref(n))
+        if p.rank == 1:
+            assert rc == capi.HG_EUNSUPPORTED
+            continue
+        assert rc == 0, capi.lib().hg_last_error()
+        assert n.value > 1000 and b"hg_apply" in buf.value
+        assert b"__fadd_rn" in buf.value or b"__dadd_rn" in buf.value
+        done += 1
+    assert done >= 4
+
+
+def test_pw_advection_program():
+    p = hg.Program.pw_advection(128, 512, 512)
+    assert p.prog.nresults == 3 and p.prog.noperands == 3 and p.prog.nfields == 6
+    assert p.core_points() == 128 * 512 * 512
+    with pytest.raises(capi.HgError, match="diagonal"):
+        p.decompose([2, 1, 1])

@@ -19,6 +19,7 @@ WL = [  # name, spec, bytes/pt, steps
     ("heat3d_so8_1024", ("heat", 3, 1024, 8), 8, 60),
     ("heat2d_so2_1024", ("heat", 2, 1024, 2), 8, 2000),
     ("heat2d_so2_16384", ("heat", 2, 16384, 2), 8, 60),
+    ("pw_advection_128x512x512", "pw", 24, 100),
 ]
 
 
@@ -33,7 +34,8 @@ def main():
     for name, spec, bpp, steps in WL:
         if only and name not in only.split(","):
             continue
-        prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+        prog = (hg.Program.pw_advection(128, 512, 512) if spec == "pw"
+                else hg.build_kernel(hg.KernelSpec(*spec, "f32")))
         plan = hg.Plan(prog)
         plan.init_fields(stream=sh)
         for ch in chunks:
