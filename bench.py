@@ -28,6 +28,23 @@ sys.path.insert(0, REPO)
 
 BYTES_PER_POINT = 8  # fp32 heat: read u_in once, write u_out once
 
+# --workload: BASELINE.json configs.  The default (config 5, weak) is the scaling line; the
+# others are single-GPU configs (replicas when N > 1), measured for DESIGN.md.
+WORKLOADS = {
+    "heat3d_weak": {"kind": "heat3d", "bpp": 8, "desc": "BASELINE config 5 (weak; N=1 = 1 GPU)"},
+    "heat3d_512": {"kind": "single", "bpp": 8, "desc": "BASELINE config 2: heat3d SDO4 512^3",
+                   "build": lambda hg: hg.build_kernel(hg.KernelSpec("heat", 3, 512, 4, "f32"))},
+    "wave3d_1024": {"kind": "single", "bpp": 12,
+                    "desc": "BASELINE config 3: wave3d SDO8 1024^3",
+                    "build": lambda hg: hg.build_kernel(hg.KernelSpec("wave", 3, 1024, 8, "f32"))},
+    "pw_advection": {"kind": "single", "bpp": 24,
+                     "desc": "BASELINE config 4: PW advection 128x512x512 (x fastest)",
+                     "build": lambda hg: hg.Program.pw_advection(128, 512, 512)},
+    "heat2d_1024": {"kind": "single", "bpp": 8,
+                    "desc": "BASELINE config 1: heat2d SDO2 1024^2 (L2-resident)",
+                    "build": lambda hg: hg.build_kernel(hg.KernelSpec("heat", 2, 1024, 2, "f32"))},
+}
+
 
 def _peaks():
     try:
@@ -109,31 +126,44 @@ def _ncu_traffic(workload):
         return None
 
 
-def cpu_baseline(extent=256, timesteps=2):
+def cpu_baseline(workload="heat3d_weak"):
     """The reference's own CPU path (oracle/_ref: the reference core compiled from its sources),
-    the `halogen bench` recipe (tools/halogen.cpp:296-318): buildKernel -> f32 -> initialFields
-    -> steady_clock around runSerialStencil.  Single-threaded by design (the interpreter is)."""
+    the `halogen bench` recipe (tools/halogen.cpp:296-318): buildKernel (or the authored module)
+    -> f32 -> initialFields -> steady_clock around runSerialStencil.  Single-threaded by design
+    (the interpreter is), on a bounded sample of the workload."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     from oracle import REF_PATH, Port, Ref
+    samples = {  # workload -> (kind, rank, extent, order, timesteps)
+        "heat3d_weak": ("heat", 3, 256, 4, 2), "heat3d_512": ("heat", 3, 256, 4, 2),
+        "wave3d_1024": ("wave", 3, 160, 8, 2), "heat2d_1024": ("heat", 2, 1024, 2, 20),
+        "pw_advection": ("pw", 3, (64, 128, 128), None, 1),
+    }
+    kind, rank, ext, order, timesteps = samples[workload]
+    pts = ext[0] * ext[1] * ext[2] if isinstance(ext, tuple) else ext ** rank
     if os.path.exists(REF_PATH):
         ref = Ref()
-        mod = ref.build("heat", 3, extent, 4, True)
+        if kind == "pw":
+            from paper_2404_02218_b200.programs.pw_advection import xir
+            mod = ref.pipeline(ref.parse(xir(*ext)), "propagate-bounds")
+        else:
+            mod = ref.build(kind, rank, ext, order, True)
         bufs = ref.L.hr_initial_fields(mod)
         secs = ref.L.hr_time_serial(mod, bufs, timesteps)
-        kind = "reference"
+        kindv = "reference"
     else:  # the C restatement, one thread
         import paper_2404_02218_b200 as hg
         port = Port()
-        prog = hg.build_kernel(hg.KernelSpec("heat", 3, extent, 4, "f32"))
+        prog = (hg.Program.pw_advection(*ext) if kind == "pw"
+                else hg.build_kernel(hg.KernelSpec(kind, rank, ext, order, "f32")))
         arrays = port.initial_fields(prog)
         t0 = time.perf_counter()
         port.run(prog, arrays, timesteps, nthreads=1)
         secs = time.perf_counter() - t0
-        kind = "port"
-    pts = extent ** 3
-    return {"value": pts * timesteps / secs / 1e9, "unit": "GPts/s", "cores": 1, "kind": kind,
-            "sample": f"heat3d so4 f32 {extent}^3 x {timesteps} timesteps, runSerialStencil, "
-                      f"1 thread (host nproc={os.cpu_count()})",
+        kindv = "port"
+    return {"value": pts * timesteps / secs / 1e9, "unit": "GPts/s", "cores": 1, "kind": kindv,
+            "sample": f"{kind}{rank}d {ext if isinstance(ext, tuple) else f'{ext}^{rank}'} "
+                      f"x {timesteps} timesteps, runSerialStencil, 1 thread (host "
+                      f"nproc={os.cpu_count()})",
             "seconds": secs}
 
 
@@ -211,13 +241,18 @@ def run_ours(args):
         gext = [E * grid[0], E * grid[1], E * grid[2]]  # E^3 per GPU
     else:
         gext = [args.strong_extent] * 3                 # fixed global domain
-    glob = hg.build_kernel(hg.KernelSpec("heat", 3, E, 4, "f32")).with_extents(gext)
-    local, dc = glob.decompose(grid)
+    wl = WORKLOADS[args.workload]
+    if wl["kind"] == "heat3d":
+        glob = hg.build_kernel(hg.KernelSpec("heat", 3, E, 4, "f32")).with_extents(gext)
+        local, dc = glob.decompose(grid)
+        origin = hd.origin_of(rank, grid, list(dc.core[:3]))
+    else:  # single-GPU BASELINE configs; N > 1 runs independent replicas
+        grid = [1] * 3
+        local, dc, origin = wl["build"](hg), None, None
     plan = hg.Plan(local, local_rank)
-    origin = hd.origin_of(rank, grid, list(dc.core[:3]))
     plan.init_fields(origin=origin, stream=sh)
     dmp = None
-    if world > 1:
+    if world > 1 and dc is not None:
         dmp = hg.Dmp(plan, dc, rank)
         hd.connect(dmp, rank, grid, world)
         dist.barrier()
@@ -229,7 +264,9 @@ def run_ours(args):
             dmp.run(k, stream=sh)
 
     core_local = local.core_points()
-    steps(args.warmup)
+    # warm-up: W steps, and at least 40 so that launch-bound configs capture their CUDA graph
+    # (hg_plan_run) before the timed region
+    steps(max(args.warmup, 40))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -260,8 +297,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     k_ms = kev0.elapsed_time(kev1) / kk
     peak, peak_src = _peaks()
-    achieved = BYTES_PER_POINT * core_local / (k_ms / 1e3) / 1e9
-    traffic = _ncu_traffic("heat3d_so4_1024")
+    bpp = WORKLOADS[args.workload]["bpp"]
+    achieved = bpp * core_local / (k_ms / 1e3) / 1e9
+    traffic = _ncu_traffic({"heat3d_weak": "r1_heat3d_so4_1024",
+                            "wave3d_1024": "r1_wave3d_so8_1024"}.get(args.workload, ""))
 
     # end to end through the public API with HOST buffers: upload -> T steps -> download
     e2e = None
@@ -316,9 +355,11 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": args.mode, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference initValue hash, buffer.cpp:142-179)",
-            "config": {"workload": f"heat3d_so4_{args.mode} (BASELINE config 5"
-                                   f"{'; N=1 is the 1-GPU case' if args.mode == 'weak' else ''})",
-                       "kernel": plan.kernel_name, "core_per_gpu": list(dc.core[:3]),
+            "config": {"workload": (f"heat3d_so4_{args.mode} (BASELINE config 5"
+                                    f"{'; N=1 is the 1-GPU case' if args.mode == 'weak' else ''})")
+                       if args.workload == "heat3d_weak" else WORKLOADS[args.workload]["desc"],
+                       "kernel": plan.kernel_name,
+                       "core_per_gpu": list(dc.core[:3]) if dc is not None else None,
                        "global_core": gext, "grid": grid, "halo": 2,
                        "l2": "inputs >> 126 MB L2 (GBs of fields per GPU), no flush needed",
                        "transport": "NVLink P2P put (CUDA IPC) + system-scope flags"
@@ -326,14 +367,14 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": plan.kernel_name, "kernel_ms": k_ms,
-                         "algorithmic_bytes_per_launch": BYTES_PER_POINT * core_local,
+                         "algorithmic_bytes_per_launch": bpp * core_local,
                          "peak_source": peak_src},
             "clocks": clocks,
             "gpu_launches": launches,
             "e2e": e2e,
         }
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline()
+            out["cpu_baseline"] = cpu_baseline(args.workload)
         print(json.dumps(out), flush=True)
     if dmp is not None:
         dmp.close()
@@ -352,6 +393,7 @@ def main():
     ap.add_argument("--grid", default=None, help="process grid AxBxC (default: weak N x 1 x 1, "
                                                  "strong 1/2x1x1/2x2x1/2x2x2)")
     ap.add_argument("--mode", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--workload", default="heat3d_weak", choices=list(WORKLOADS))
     ap.add_argument("--strong-extent", type=int, default=2048)
     ap.add_argument("--e2e-timesteps", type=int, default=100)
     ap.add_argument("--e2e-calls", type=int, default=2)

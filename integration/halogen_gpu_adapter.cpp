@@ -22,6 +22,7 @@
 #include "halogen/exec/serial.hpp"
 #include "halogen/exec/simulator.hpp"
 #include "halogen/ir/diagnostics.hpp"
+#include "halogen/ir/pass.hpp"
 
 #include <cstring>
 #include <memory>
@@ -88,10 +89,56 @@ std::vector<std::shared_ptr<Buffer>> runSerialStencil(ir::Operation &module,
   return out;
 }
 
+namespace {
+
+// The module `halogen bench --grid` times is lowered past dmp
+// ("propagate-bounds,decompose grid=G,lower-dmp-to-mpi", tools/halogen.cpp:320-323): its
+// @run(%T, fields...) holds the swap as pack loops + mpi.isend/irecv/waitall + unpack loops
+// (mpi_transforms.cpp:148-419).  Its dmp-level form is recovered from the module's own
+// dmp.reference snapshot and dmp.topology, and accepted only if lowering it again reproduces
+// the given module exactly (ir::structurallyEqual) -- then both compute the same fields (the
+// reference pins every level bitwise, exec_tests.cpp:148-190).
+ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
+  const ir::Operation *run = ir::lookupFunc(module, "run");
+  if (!run || run->regions.empty() || run->regions[0].args.empty() ||
+      !run->regions[0].args[0].type.isScalar(ir::Scalar::Index))
+    return nullptr; // not a lowered module
+  auto geom = geometryOf(module);
+  if (!geom.ok()) {
+    err = geom.diagText();
+    return nullptr;
+  }
+  std::string grid;
+  for (std::size_t d = 0; d < geom->grid.size(); ++d)
+    grid += (d ? "x" : "") + std::to_string(geom->grid[d]);
+  for (const char *extra : {"", ",eliminate-redundant-swaps"}) {
+    auto dmp = ir::runPipeline(*geom->reference,
+                               std::string("propagate-bounds,decompose grid=") + grid + extra);
+    if (!dmp.ok())
+      continue;
+    auto low = ir::runPipeline(**dmp, "lower-dmp-to-mpi");
+    if (low.ok() && ir::structurallyEqual(**low, module))
+      return std::move(*dmp);
+  }
+  err = "lowered module is not the lower-dmp-to-mpi form of its dmp.reference; the device "
+        "path executes stencil/dmp-level modules";
+  return nullptr;
+}
+
+} // namespace
+
 SimResult simulate(ir::Operation &module, const std::vector<std::shared_ptr<Buffer>> &globalInit,
                    const SimOptions &opts) {
   SimResult res;
   try {
+    std::string lerr;
+    ir::ModuleOp dmpLevel = dmpLevelOf(module, lerr);
+    if (!lerr.empty()) {
+      res.error = lerr;
+      return res;
+    }
+    if (dmpLevel)
+      return halogen::exec::gpu::simulate(*dmpLevel, globalInit, opts);
     auto geom = geometryOf(module);
     if (!geom.ok()) {
       res.error = geom.diagText();

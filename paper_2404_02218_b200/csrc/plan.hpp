@@ -5,6 +5,7 @@
 #include "jit.hpp"
 #include "kernels.hpp"
 
+#include <map>
 #include <memory>
 #include <vector>
 
@@ -31,6 +32,7 @@ struct hg_plan {
   hg::StarLaunch fuse{};              // one-shot: fused-swap fields (fuse.fuse != 0)
   std::shared_ptr<hg::JitKernel> jit;  // fused-apply family (generated, per program)
   std::vector<CUtensorMap> tmApply;   // per buffer, for the fused-apply boxes
+  std::map<int, cudaGraphExec_t> graphs; // hg_plan_run: captured G-step graphs per phase
 };
 
 namespace hg {

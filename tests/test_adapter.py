@@ -68,6 +68,24 @@ def test_simulate_dropin(ref, adapter, spec, grid, T):
     assert _fps(ref, gpu) == _fps(ref, cpu)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec,grid,T", [
+    (("heat", 2, 12, 2), "2x2", 3), (("heat", 3, 32, 4), "2x2x2", 2),
+    (("wave", 3, 24, 8), "3x1x1", 3),
+])
+def test_simulate_lowered_mpi_module(ref, adapter, spec, grid, T):
+    # the exact module `halogen bench --grid` times: propagate-bounds,decompose,lower-dmp-to-mpi
+    mod = ref.build(*spec, True)
+    low = ref.pipeline(mod, "propagate-bounds,decompose grid=" + grid + ",lower-dmp-to-mpi")
+    init = ref.L.hr_initial_fields(mod)
+    cpu = ref.L.hr_simulate(low, init, T, 0)
+    assert cpu, ref.err()
+    err = C.create_string_buffer(512)
+    gpu = adapter.hga_simulate(low, init, T, err, 512)
+    assert gpu, err.value.decode()
+    assert _fps(ref, gpu) == _fps(ref, cpu)
+
+
 def test_adapter_errors_like_the_reference(ref, adapter):
     # wrong field count -> TrapError text (serial.cpp:68-69 analogue), never a crash
     mod = ref.build("heat", 2, 8, 2, True)
