@@ -89,8 +89,6 @@ std::vector<std::shared_ptr<Buffer>> runSerialStencil(ir::Operation &module,
   return out;
 }
 
-namespace {
-
 // The module `halogen bench --grid` times is lowered past dmp
 // ("propagate-bounds,decompose grid=G,lower-dmp-to-mpi", tools/halogen.cpp:320-323): its
 // @run(%T, fields...) holds the swap as pack loops + mpi.isend/irecv/waitall + unpack loops
@@ -111,21 +109,20 @@ ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
   std::string grid;
   for (std::size_t d = 0; d < geom->grid.size(); ++d)
     grid += (d ? "x" : "") + std::to_string(geom->grid[d]);
-  for (const char *extra : {"", ",eliminate-redundant-swaps"}) {
-    auto dmp = ir::runPipeline(*geom->reference,
-                               std::string("propagate-bounds,decompose grid=") + grid + extra);
-    if (!dmp.ok())
-      continue;
-    auto low = ir::runPipeline(**dmp, "lower-dmp-to-mpi");
-    if (low.ok() && ir::structurallyEqual(**low, module))
-      return std::move(*dmp);
-  }
+  // the snapshot was taken inside `decompose`, i.e. after whatever ran before it
+  for (const char *pre : {"decompose grid=", "propagate-bounds,decompose grid="})
+    for (const char *extra : {"", ",eliminate-redundant-swaps"}) {
+      auto dmp = ir::runPipeline(*geom->reference, std::string(pre) + grid + extra);
+      if (!dmp.ok())
+        continue;
+      auto low = ir::runPipeline(**dmp, "lower-dmp-to-mpi");
+      if (low.ok() && ir::structurallyEqual(**low, module))
+        return std::move(*dmp);
+    }
   err = "lowered module is not the lower-dmp-to-mpi form of its dmp.reference; the device "
         "path executes stencil/dmp-level modules";
   return nullptr;
 }
-
-} // namespace
 
 SimResult simulate(ir::Operation &module, const std::vector<std::shared_ptr<Buffer>> &globalInit,
                    const SimOptions &opts) {
@@ -225,6 +222,18 @@ void *hga_run_serial(void *mod, void *bufs, long long timesteps, char *err, int 
     std::snprintf(err, static_cast<size_t>(cap), "%s", e.what());
     return nullptr;
   }
+}
+
+// 1 when a lowered (@run) module is recognised as the lower-dmp-to-mpi form of its own
+// dmp.reference, 0 for dmp/stencil-level modules, -1 (err set) when it is not.
+int hga_lowered_recognised(void *mod, char *err, int cap) {
+  std::string e;
+  auto m = halogen::exec::gpu::dmpLevelOf(*static_cast<hg_ref::Mod *>(mod)->m, e);
+  if (!e.empty()) {
+    std::snprintf(err, static_cast<size_t>(cap), "%s", e.c_str());
+    return -1;
+  }
+  return m ? 1 : 0;
 }
 
 void *hga_simulate(void *mod, void *global_init, long long timesteps, char *err, int cap) {

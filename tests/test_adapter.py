@@ -20,7 +20,20 @@ def adapter(ref):
         f = getattr(L, n)
         f.restype = C.c_void_p
         f.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_char_p, C.c_int]
+    L.hga_lowered_recognised.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
     return L
+
+
+@pytest.mark.parametrize("spec,grid", [(("heat", 2, 12, 2), "2x2"), (("wave", 3, 24, 8), "3x1x1"),
+                                       (("heat", 3, 32, 4), "2x2x2"), (("wave", 1, 16, 4), "4")])
+def test_lowered_module_recognised(ref, adapter, spec, grid):
+    # the `halogen bench --grid` module (tools/halogen.cpp:320-323) maps back to its dmp level
+    mod = ref.build(*spec, True)
+    err = C.create_string_buffer(300)
+    low = ref.pipeline(mod, f"propagate-bounds,decompose grid={grid},lower-dmp-to-mpi")
+    assert adapter.hga_lowered_recognised(low, err, 300) == 1, err.value
+    dmp = ref.pipeline(mod, f"propagate-bounds,decompose grid={grid}")
+    assert adapter.hga_lowered_recognised(dmp, err, 300) == 0
 
 
 def test_adapter_loads_and_exports(adapter):
