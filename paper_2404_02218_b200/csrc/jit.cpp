@@ -447,7 +447,8 @@ int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
   int ny = r == 3 ? int(p.store[0].ub[1] - p.store[0].lb[1]) : 1;
   int nx = int(p.store[0].ub[r - 1] - p.store[0].lb[r - 1]);
   int tiles_x = (nx + K.tx - 1) / K.tx, tiles_y = (ny + K.ty - 1) / K.ty;
-  int nch = chunks > 0 ? chunks : std::max(1, (nz + 32) / 64);
+  // z-chunks of ~32 planes (measured best for the PW set: 4 chunks at nz=128)
+  int nch = chunks > 0 ? chunks : std::max(1, (nz + 16) / 32);
   int chunk = (nz + nch - 1) / nch;
   nch = (nz + chunk - 1) / chunk;
   int iv[10] = {zs, ys, xs, nz, ny, nx, tiles_x, tiles_y, chunk, nch};
