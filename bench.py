@@ -299,7 +299,7 @@ def run_ours(args):
     peak, peak_src = _peaks()
     bpp = WORKLOADS[args.workload]["bpp"]
     achieved = bpp * core_local / (k_ms / 1e3) / 1e9
-    traffic = _ncu_traffic({"heat3d_weak": "r1_heat3d_so4_1024",
+    traffic = _ncu_traffic({"heat3d_weak": "r1_heat3d_so4_1024", "pw_advection": "r1_pw_advection_128x512x512",
                             "wave3d_1024": "r1_wave3d_so8_1024"}.get(args.workload, ""))
 
     # end to end through the public API with HOST buffers: upload -> T steps -> download
