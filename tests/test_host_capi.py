@@ -154,3 +154,24 @@ def test_pw_advection_program():
     assert p.core_points() == 128 * 512 * 512
     with pytest.raises(capi.HgError, match="diagonal"):
         p.decompose([2, 1, 1])
+
+
+def test_no_fma_in_stencil_kernels():
+    # the bit-exactness contract (no FMA contraction, proj/CMakeLists.txt:8-10) checked on the
+    # shipped SASS: the star kernels carry no FFMA/DFMA/FFMA2 at all; only the generic kernel's
+    # correctly rounded division (__fdiv_rn/__ddiv_rn expansion) may use fused steps
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not on PATH")
+    sass = subprocess.run(["cuobjdump", "-sass", capi.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    fn, bad, seen = None, [], 0
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+            seen += "starKernel" in fn
+        elif fn and "starKernel" in fn and any(op in line for op in ("FFMA", "DFMA", "HFMA")):
+            bad.append((fn, line.strip()))
+    assert seen >= 24
+    assert not bad, bad[:3]
