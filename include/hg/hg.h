@@ -173,6 +173,14 @@ int hg_exchanges(int n, const int64_t *core, const int64_t *below, const int64_t
 int hg_build_kernel_program(const char *kind, int rank, int64_t extent, int order, int dtype,
                             hg_program *prog, hg_op *ops, int cap_ops);
 
+/* Reads the stencil-level textual IR (the reference's `.xir` syntax, printer.cpp/parser.cpp):
+ * one all-field func.func with stencil.load / dmp.swap / one stencil.apply / stencil.store.
+ * Writes the program (+ ops[cap_ops]); for a decomposed module also *decomp and
+ * *decomposed = 1.  The module's dmp.reference text (the pre-decompose snapshot) is copied
+ * into reference[ref_cap] when given.  Errors carry "<xir>:line:col: message". */
+int hg_parse_program(const char *text, hg_program *prog, hg_op *ops, int cap_ops,
+                     hg_decomp *decomp, int *decomposed, char *reference, size_t ref_cap);
+
 /* Validates a program; on HG_OK writes the kernel family that would run it
  * ("star3d_r2_heat", "generic", ...) into name[cap]. No GPU needed. */
 int hg_program_match(const hg_program *prog, char *name, size_t cap);
@@ -213,6 +221,8 @@ int hg_plan_unpack(hg_plan *plan, int buffer, const int64_t *at, const int64_t *
 /* Tuning knobs of the star family: z-chunks per column tile (0 = auto) and whether the
  * z-boundary chunks run last (lets halo exchange overlap interior compute). */
 int hg_plan_set_tuning(hg_plan *plan, int chunks, int boundary_last);
+/* Block until all work queued for the plan's device has finished. */
+int hg_plan_synchronize(hg_plan *plan);
 /* Kernel launches issued by this plan so far (for bench/gpu_launches accounting). */
 int64_t hg_plan_launch_count(const hg_plan *plan);
 

@@ -173,6 +173,19 @@ class Program:
         return Program(p, ops)
 
     @staticmethod
+    def parse(text: str):
+        """Read `.xir` text (hg_parse_program).  Returns (Program, HgDecomp or None,
+        dmp.reference text)."""
+        ops = (HgOp * capi.HG_MAX_OPS)()
+        prog = HgProgram()
+        dc = HgDecomp()
+        dec = C.c_int()
+        ref = C.create_string_buffer(1 << 20)
+        check(lib().hg_parse_program(text.encode(), C.byref(prog), ops, capi.HG_MAX_OPS,
+                                     C.byref(dc), C.byref(dec), ref, 1 << 20))
+        return Program(prog, ops), (dc if dec.value else None), ref.value.decode()
+
+    @staticmethod
     def pw_advection(nz: int, ny: int, nx: int) -> "Program":
         """BASELINE config 4: the authored PW-advection program (programs/pw_advection.py),
         as exported by the reference's parser, resized to nz x ny x nx."""

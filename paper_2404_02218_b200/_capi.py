@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
                                               P(HgProgram), P(HgOp), C.c_int]),
         "hg_program_match": (C.c_int, [P(HgProgram), C.c_char_p, SZ]),
         "hg_apply_compile": (C.c_int, [P(HgProgram), C.c_char_p, SZ, P(SZ)]),
+        "hg_parse_program": (C.c_int, [C.c_char_p, P(HgProgram), P(HgOp), C.c_int, P(HgDecomp),
+                                       P(C.c_int), C.c_char_p, SZ]),
         "hg_decompose_program": (C.c_int, [P(HgProgram), C.c_int, P(I64), P(HgProgram),
                                            P(HgDecomp)]),
         "hg_plan_create": (C.c_int, [P(HgProgram), C.c_int, P(V)]),
@@ -117,6 +119,7 @@ def lib() -> C.CDLL:
         "hg_plan_pack": (C.c_int, [V, C.c_int, P(I64), P(I64), V, V]),
         "hg_plan_unpack": (C.c_int, [V, C.c_int, P(I64), P(I64), V, V]),
         "hg_plan_launch_count": (I64, [V]),
+        "hg_plan_synchronize": (C.c_int, [V]),
         "hg_plan_set_tuning": (C.c_int, [V, C.c_int, C.c_int]),
         "hg_dmp_create": (C.c_int, [V, P(HgDecomp), I64, P(V)]),
         "hg_dmp_destroy": (C.c_int, [V]),

@@ -535,6 +535,15 @@ int hg_plan_unpack(hg_plan *p, int b, const int64_t *at, const int64_t *size, co
 
 int64_t hg_plan_launch_count(const hg_plan *p) { return p ? p->launches : 0; }
 
+int hg_plan_synchronize(hg_plan *p) {
+  if (!p)
+    return setError(HG_EINVAL, "null plan");
+  int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice");
+  if (st)
+    return st;
+  return cudaCheck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+}
+
 int hg_plan_set_tuning(hg_plan *p, int chunks, int boundary_last) {
   if (!p || chunks < 0)
     return setError(HG_EINVAL, "bad tuning");

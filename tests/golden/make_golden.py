@@ -215,6 +215,7 @@ def main():
             raise RuntimeError(ref.err())
         serial.append({"spec": [kind, rank, ext, order, f32], "T": T,
                        "program": prog_json(prog, ops),
+                       "text": ref.print(mod) if ext <= 40 else None,
                        "init_fp": fps(ref, init), "final_fp": fps(ref, fin),
                        "seconds": time.time() - t0})
         for b in (init, work, fin):
@@ -235,6 +236,7 @@ def main():
         if not fin:
             raise RuntimeError(ref.err())
         auth.append({"name": name, "T": T, "program": prog_json(prog, ops),
+                     "text": ref.print(mod),
                      "init_fp": fps(ref, init), "final_fp": fps(ref, fin)})
         if name == "pw_advection_16x24x40":  # the authored config-4 program, as data
             with open(os.path.join(REPO, "paper_2404_02218_b200", "programs",
@@ -264,6 +266,7 @@ def main():
             raise RuntimeError(ref.err())
         dec.append({"spec": [kind, rank, ext, order, f32], "grid": grid, "T": T,
                     "local_program": prog_json(lprog, lops), "decomp": decomp_json(dc),
+                    "text": ref.print(dmod),
                     "sim_fp": fps(ref, res), "mpi_sim_fp": fps(ref, mres),
                     "serial_fp": fps(ref, ser)})
         print("decomp", kind, rank, ext, order, grid, T, flush=True)

@@ -176,3 +176,35 @@ def test_no_fma_in_stencil_kernels():
             bad.append((fn, line.strip()))
     assert seen >= 24
     assert not bad, bad[:3]
+
+
+def test_native_xir_reader_matches_reference_parser(golden):
+    # hg_parse_program reads the reference's printed modules into the same descriptors the
+    # reference's own parser + IR walk produce (serial, authored, decomposed + swaps)
+    n = 0
+    for c in golden["serial"] + golden["authored"]:
+        if not c.get("text"):
+            continue
+        prog, dc, _ = hg.Program.parse(c["text"])
+        assert prog_to_json(prog) == c["program"], c.get("name", c.get("spec"))
+        assert dc is None
+        n += 1
+    for c in golden["decomposed"]:
+        prog, dc, reftext = hg.Program.parse(c["text"])
+        assert prog_to_json(prog) == c["local_program"]
+        assert decomp_to_json(dc) == c["decomp"]
+        glob, _, _ = hg.Program.parse(reftext)        # the dmp.reference snapshot
+        assert glob.core_points() == prog.core_points() * int(np.prod(c["grid"]))
+        n += 1
+    assert n >= 30
+
+
+def test_native_xir_reader_errors():
+    with pytest.raises(capi.HgError, match="<xir>:1:1"):
+        hg.Program.parse("module {}")
+    bad = ("builtin.module {\n  func.func @f(%a : !field<[0,4]xf32>, %b : !field<[0,4]xf32>) {\n"
+           "    %t = stencil.load %a : !field<[0,4]xf32> -> !temp<?xf32>\n"
+           "    %o = stencil.apply(%x = %t : !temp<?xf32>) -> !temp<?xf32> {\n"
+           "      %v = arith.addf %x, %x : f32\n      stencil.return %v : f32\n    }\n")
+    with pytest.raises(capi.HgError, match="use before def"):
+        hg.Program.parse(bad)
