@@ -23,6 +23,7 @@
 #include "halogen/exec/simulator.hpp"
 #include "halogen/ir/diagnostics.hpp"
 #include "halogen/ir/pass.hpp"
+#include "halogen/ir/printer.hpp"
 
 #include <cstring>
 #include <memory>
@@ -94,7 +95,7 @@ std::vector<std::shared_ptr<Buffer>> runSerialStencil(ir::Operation &module,
 // @run(%T, fields...) holds the swap as pack loops + mpi.isend/irecv/waitall + unpack loops
 // (mpi_transforms.cpp:148-419).  Its dmp-level form is recovered from the module's own
 // dmp.reference snapshot and dmp.topology, and accepted only if lowering it again reproduces
-// the given module exactly (ir::structurallyEqual) -- then both compute the same fields (the
+// the given module exactly (same printed form) -- then both compute the same fields (the
 // reference pins every level bitwise, exec_tests.cpp:148-190).
 ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
   const ir::Operation *run = ir::lookupFunc(module, "run");
@@ -106,6 +107,7 @@ ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
     err = geom.diagText();
     return nullptr;
   }
+  const std::string printed = ir::printModule(module);
   std::string grid;
   for (std::size_t d = 0; d < geom->grid.size(); ++d)
     grid += (d ? "x" : "") + std::to_string(geom->grid[d]);
@@ -116,7 +118,9 @@ ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
       if (!dmp.ok())
         continue;
       auto low = ir::runPipeline(**dmp, "lower-dmp-to-mpi");
-      if (low.ok() && ir::structurallyEqual(**low, module))
+      // compare printed forms: structurallyEqual would also see the interpreter's lazily
+      // assigned value slots (ir.cpp:284-290) if the module was already executed
+      if (low.ok() && ir::printModule(**low) == printed)
         return std::move(*dmp);
     }
   err = "lowered module is not the lower-dmp-to-mpi form of its dmp.reference; the device "

@@ -32,6 +32,10 @@ def test_lowered_module_recognised(ref, adapter, spec, grid):
     err = C.create_string_buffer(300)
     low = ref.pipeline(mod, f"propagate-bounds,decompose grid={grid},lower-dmp-to-mpi")
     assert adapter.hga_lowered_recognised(low, err, 300) == 1, err.value
+    # also after the reference interpreter has run it (value slots get numbered lazily)
+    init = ref.L.hr_initial_fields(mod)
+    assert ref.L.hr_simulate(low, init, 2, 0)
+    assert adapter.hga_lowered_recognised(low, err, 300) == 1, err.value
     dmp = ref.pipeline(mod, f"propagate-bounds,decompose grid={grid}")
     assert adapter.hga_lowered_recognised(dmp, err, 300) == 0
 
