@@ -53,6 +53,9 @@ extern "C" {
 #define HG_MAX_RESULTS 8
 #define HG_MAX_OPS 4096
 #define HG_MAX_EXCHANGES 6
+#define HG_MAX_APPLIES 32
+#define HG_MAX_TEMPS 64
+#define HG_MAX_STORES 16
 
 typedef enum hg_status {
   HG_OK = 0,
@@ -90,6 +93,20 @@ typedef struct hg_bounds {
   int64_t ub[HG_MAX_RANK];
 } hg_bounds;
 
+/* One stencil.apply of a multi-apply step (an apply may consume earlier applies' results;
+ * the reference evaluates such a producer over its whole result bounds into a temp,
+ * stencil_transforms.cpp:334-379, interpreter.cpp:713-758). */
+typedef struct hg_apply {
+  int32_t noperands;
+  int32_t operand[HG_MAX_FIELDS]; /* >= 0: field argument (stencil.load); < 0: temp (-t-1) */
+  int32_t op_begin, nops;         /* region = ops[op_begin .. op_begin+nops); operand indices
+                                     inside the region are region-relative */
+  int32_t nresults;
+  int32_t result_op[HG_MAX_RESULTS];   /* region-relative op index returned as result r */
+  int32_t result_temp[HG_MAX_RESULTS]; /* temp defined by result r */
+  hg_bounds domain;               /* evaluation domain = bounds of its result temps */
+} hg_apply;
+
 /* A stencil-level step function: fields (arguments), one apply, its stores, time slots. */
 typedef struct hg_program {
   int32_t rank;    /* 1..3 */
@@ -107,6 +124,17 @@ typedef struct hg_program {
   int32_t ngroups;                       /* stencil.time_slots (stencil_transforms.cpp:196-242) */
   int32_t group_len[HG_MAX_FIELDS];
   int32_t groups[HG_MAX_FIELDS];         /* groups flattened, group_len[i] entries each */
+  /* Multi-apply steps (napplies > 0): nops/ops hold every apply's region back to back and
+   * noperands/operand_field list the stencil.load fields in step order (decompose puts a swap
+   * before each); result_op..store above are unused; the applies run in order and the stores
+   * copy temps into fields. */
+  int32_t napplies;
+  const hg_apply *applies;               /* caller-owned, napplies entries */
+  int32_t ntemps;
+  int32_t nstores;
+  int32_t mstore_temp[HG_MAX_STORES];    /* stencil.store of this temp ... */
+  int32_t mstore_field[HG_MAX_STORES];   /* ... into this field argument ... */
+  hg_bounds mstore[HG_MAX_STORES];       /* ... over this region */
 } hg_program;
 
 /* #dmp.exchange<at size source offset to> (attributes.hpp:69-75), buffer-local raw coords. */
@@ -174,12 +202,14 @@ int hg_build_kernel_program(const char *kind, int rank, int64_t extent, int orde
                             hg_program *prog, hg_op *ops, int cap_ops);
 
 /* Reads the stencil-level textual IR (the reference's `.xir` syntax, printer.cpp/parser.cpp):
- * one all-field func.func with stencil.load / dmp.swap / one stencil.apply / stencil.store.
+ * one all-field func.func with stencil.load / dmp.swap / stencil.apply (one, or several that
+ * may consume each other -> the multi-apply form, applies[cap_applies]) / stencil.store.
  * Writes the program (+ ops[cap_ops]); for a decomposed module also *decomp and
  * *decomposed = 1.  The module's dmp.reference text (the pre-decompose snapshot) is copied
  * into reference[ref_cap] when given.  Errors carry "<xir>:line:col: message". */
 int hg_parse_program(const char *text, hg_program *prog, hg_op *ops, int cap_ops,
-                     hg_decomp *decomp, int *decomposed, char *reference, size_t ref_cap);
+                     hg_apply *applies, int cap_applies, hg_decomp *decomp, int *decomposed,
+                     char *reference, size_t ref_cap);
 
 /* Validates a program; on HG_OK writes the kernel family that would run it
  * ("star3d_r2_heat", "generic", ...) into name[cap]. No GPU needed. */
@@ -192,7 +222,10 @@ int hg_apply_compile(const hg_program *prog, char *src, size_t cap, size_t *cubi
 
 /* The decompose pass on a program (dmp_transforms.cpp:101-312): rewrites *local (field bounds
  * = rank-0 core widened by the halos, stores = rank-0 core) and fills *decomp (one swap per
- * apply operand load, template exchanges).  `local` may alias `global`. */
+ * stencil.load, template exchanges).  `local` may alias `global` for single-apply programs;
+ * for a multi-apply program (no apply may read another's result, as in the reference) the
+ * caller sets local->applies to a buffer of global->napplies entries, which receives the
+ * applies with their domains rewritten to the local core. */
 int hg_decompose_program(const hg_program *global, int ndim, const int64_t *grid,
                          hg_program *local, hg_decomp *decomp);
 

@@ -25,6 +25,7 @@
 #include "halogen/ir/pass.hpp"
 #include "halogen/ir/printer.hpp"
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -67,6 +68,7 @@ std::vector<std::shared_ptr<Buffer>> runSerialStencil(ir::Operation &module,
     throw ir::TrapError("", e.what());
   }
   c.prog.ops = c.ops.data();
+  c.prog.applies = c.applies.empty() ? nullptr : c.applies.data();
   if (static_cast<int>(fields.size()) != c.prog.nfields)
     throw ir::TrapError("", "field count does not match the function");
   for (int i = 0; i < c.prog.nfields; ++i)
@@ -97,6 +99,39 @@ std::vector<std::shared_ptr<Buffer>> runSerialStencil(ir::Operation &module,
 // dmp.reference snapshot and dmp.topology, and accepted only if lowering it again reproduces
 // the given module exactly (same printed form) -- then both compute the same fields (the
 // reference pins every level bitwise, exec_tests.cpp:148-190).
+// Printed form with each run of consecutive memref.dealloc lines sorted: lower-dmp-to-mpi
+// emits the end-of-function deallocations in the order of a std::map keyed by swap-op pointers
+// (mpi_transforms.cpp:239,406-410), i.e. heap-address order, so two lowerings of one dmp
+// module may differ only there.
+std::string canonicalPrint(ir::Operation &module) {
+  const std::string text = ir::printModule(module);
+  std::vector<std::string> lines, run;
+  std::string out;
+  size_t at = 0;
+  auto flush = [&] {
+    std::sort(run.begin(), run.end());
+    for (auto &l : run)
+      out += l + "\n";
+    run.clear();
+  };
+  while (at < text.size()) {
+    size_t e = text.find('\n', at);
+    if (e == std::string::npos)
+      e = text.size();
+    std::string line = text.substr(at, e - at);
+    at = e + 1;
+    size_t b = line.find_first_not_of(' ');
+    if (b != std::string::npos && line.compare(b, 14, "memref.dealloc") == 0) {
+      run.push_back(line);
+      continue;
+    }
+    flush();
+    out += line + "\n";
+  }
+  flush();
+  return out;
+}
+
 ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
   const ir::Operation *run = ir::lookupFunc(module, "run");
   if (!run || run->regions.empty() || run->regions[0].args.empty() ||
@@ -107,7 +142,7 @@ ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
     err = geom.diagText();
     return nullptr;
   }
-  const std::string printed = ir::printModule(module);
+  const std::string printed = canonicalPrint(module);
   std::string grid;
   for (std::size_t d = 0; d < geom->grid.size(); ++d)
     grid += (d ? "x" : "") + std::to_string(geom->grid[d]);
@@ -120,7 +155,7 @@ ir::ModuleOp dmpLevelOf(ir::Operation &module, std::string &err) {
       auto low = ir::runPipeline(**dmp, "lower-dmp-to-mpi");
       // compare printed forms: structurallyEqual would also see the interpreter's lazily
       // assigned value slots (ir.cpp:284-290) if the module was already executed
-      if (low.ok() && ir::printModule(**low) == printed)
+      if (low.ok() && canonicalPrint(**low) == printed)
         return std::move(*dmp);
     }
   err = "lowered module is not the lower-dmp-to-mpi form of its dmp.reference; the device "
@@ -148,6 +183,7 @@ SimResult simulate(ir::Operation &module, const std::vector<std::shared_ptr<Buff
     const DecompGeometry &G = *geom;
     hg_ir::Converted c = hg_ir::convert(module);
     c.prog.ops = c.ops.data();
+    c.prog.applies = c.applies.empty() ? nullptr : c.applies.data();
     if (!c.decomposed) {
       res.error = "module is not decomposed";
       return res;

@@ -27,6 +27,7 @@ namespace hg_ir {
 struct Converted {
   hg_program prog{};
   std::vector<hg_op> ops;
+  std::vector<hg_apply> applies; // multi-apply steps (prog.applies points here)
   bool decomposed = false;
   hg_decomp decomp{};
 };
@@ -55,6 +56,158 @@ inline void boundsOf(const halogen::ir::Bounds &b, hg_bounds &out) {
     out.lb[d] = b.dims[d].lb;
     out.ub[d] = b.dims[d].ub;
   }
+}
+
+inline void timeSlotsInto(const halogen::ir::Operation &module, hg_program &p) {
+  using namespace halogen::ir;
+  if (const Attribute *ts = module.attr("stencil.time_slots")) {
+    const auto &outer = ts->as<ArrayAttr>();
+    int at = 0;
+    for (const Attribute &g : outer.elems) {
+      std::vector<std::int64_t> idx;
+      attrToIndexVector(g, idx);
+      p.group_len[p.ngroups++] = static_cast<int>(idx.size());
+      for (auto i : idx)
+        p.groups[at++] = static_cast<int>(i);
+    }
+  }
+}
+
+// Steps with several applies, or an apply consuming another: every apply is evaluated over its
+// result bounds into temps (materializeApply, stencil_transforms.cpp:334-379).
+// dmp.swap {grid, exchanges} (dmp_ops.cpp) -> one hg_swap of the decomposition
+inline void swapInto(const halogen::ir::Operation &op, Converted &c) {
+  using namespace halogen::ir;
+  c.decomposed = true;
+  if (c.decomp.nswaps >= HG_MAX_FIELDS)
+    throw std::runtime_error("too many swaps");
+  hg_swap &s = c.decomp.swaps[c.decomp.nswaps++];
+  s.field = op.operands[0]->argIdx;
+  const auto *g = op.attr("grid")->dynAs<GridAttr>();
+  c.decomp.ndim = static_cast<int>(g->dims.size());
+  for (int d = 0; d < c.decomp.ndim; ++d)
+    c.decomp.grid[d] = g->dims[static_cast<std::size_t>(d)];
+  const auto *xs = op.attr("exchanges")->dynAs<ArrayAttr>();
+  s.nexchanges = 0;
+  for (const Attribute &a : xs->elems) {
+    const auto &e = a.as<ExchangeAttr>();
+    hg_exchange &x = s.ex[s.nexchanges++];
+    for (std::size_t d = 0; d < e.at.size(); ++d) {
+      x.at[d] = e.at[d];
+      x.size[d] = e.size[d];
+      x.offset[d] = e.offset[d];
+      x.to[d] = e.to[d];
+    }
+  }
+}
+
+inline Converted convertMulti(const halogen::ir::Operation &module,
+                              const halogen::ir::Operation *entry, Converted c) {
+  using namespace halogen::ir;
+  const Region &body = entry->regions[0];
+  hg_program &p = c.prog;
+  std::map<const Value *, int> loadOf, tempOf;
+  for (const auto &opPtr : body.ops) {
+    const Operation &op = *opPtr;
+    if (op.name == "stencil.load") {
+      if (!op.operands[0]->isArg())
+        throw std::runtime_error("stencil.load of a non-argument");
+      if (p.noperands >= HG_MAX_FIELDS)
+        throw std::runtime_error("too many loads");
+      loadOf[&op.results[0]] = op.operands[0]->argIdx;
+      p.operand_field[p.noperands++] = op.operands[0]->argIdx; // the load list
+    } else if (op.name == "dmp.swap") {
+      swapInto(op, c);
+    } else if (op.name == "stencil.apply") {
+      if (c.applies.size() >= HG_MAX_APPLIES)
+        throw std::runtime_error("too many applies");
+      hg_apply a;
+      std::memset(&a, 0, sizeof a);
+      a.noperands = op.numOperands();
+      for (int k = 0; k < a.noperands; ++k) {
+        const Value *v = op.operands[static_cast<std::size_t>(k)];
+        if (loadOf.count(v))
+          a.operand[k] = loadOf.at(v);
+        else if (tempOf.count(v))
+          a.operand[k] = -tempOf.at(v) - 1;
+        else
+          throw std::runtime_error("apply operand is neither a load nor an apply result");
+      }
+      const auto &tt = op.results[0].type.as<TempType>();
+      if (!tt.bounds)
+        throw std::runtime_error("unresolved stencil.apply bounds (run propagate-bounds)");
+      boundsOf(*tt.bounds, a.domain);
+      a.op_begin = static_cast<int>(c.ops.size());
+      const Region &ar = op.regions[0];
+      std::map<const Value *, int> vid, argIdx;
+      for (std::size_t k = 0; k < ar.args.size(); ++k)
+        argIdx[&ar.args[k]] = static_cast<int>(k);
+      for (const auto &inPtr : ar.ops) {
+        const Operation &in = *inPtr;
+        hg_op h;
+        std::memset(&h, 0, sizeof h);
+        if (in.name == "stencil.access") {
+          h.code = HG_OP_ACCESS;
+          h.operand = argIdx.at(in.operands[0]);
+          std::vector<std::int64_t> off;
+          attrToIndexVector(*in.attr("offsets"), off);
+          for (std::size_t d = 0; d < off.size(); ++d)
+            h.off[d] = off[d];
+        } else if (in.name == "arith.constant") {
+          h.code = HG_OP_CONST;
+          h.bits = in.attr("value")->as<FloatAttr>().bits;
+        } else if (in.name == "arith.addf" || in.name == "arith.subf" ||
+                   in.name == "arith.mulf" || in.name == "arith.divf") {
+          h.code = in.name == "arith.addf"   ? HG_OP_ADD
+                   : in.name == "arith.subf" ? HG_OP_SUB
+                   : in.name == "arith.mulf" ? HG_OP_MUL
+                                             : HG_OP_DIV;
+          h.a = vid.at(in.operands[0]);
+          h.b = vid.at(in.operands[1]);
+        } else if (in.name == "stencil.return") {
+          a.nresults = in.numOperands();
+          for (int k = 0; k < a.nresults; ++k)
+            a.result_op[k] = vid.at(in.operands[static_cast<std::size_t>(k)]);
+          continue;
+        } else {
+          throw std::runtime_error("unsupported op in apply region: " + in.name);
+        }
+        vid[&in.results[0]] = static_cast<int>(c.ops.size()) - a.op_begin;
+        c.ops.push_back(h);
+      }
+      a.nops = static_cast<int>(c.ops.size()) - a.op_begin;
+      for (int k = 0; k < op.numResults(); ++k) {
+        a.result_temp[k] = p.ntemps;
+        tempOf[&op.results[static_cast<std::size_t>(k)]] = p.ntemps++;
+      }
+      c.applies.push_back(a);
+    } else if (op.name == "stencil.store") {
+      if (p.nstores >= HG_MAX_STORES)
+        throw std::runtime_error("too many stores");
+      const int k = p.nstores++;
+      p.mstore_temp[k] = tempOf.at(op.operands[0]);
+      p.mstore_field[k] = op.operands[1]->argIdx;
+      std::vector<std::int64_t> lb, ub;
+      attrToIndexVector(*op.attr("lb"), lb);
+      attrToIndexVector(*op.attr("ub"), ub);
+      for (std::size_t d = 0; d < lb.size(); ++d) {
+        p.mstore[k].lb[d] = lb[d];
+        p.mstore[k].ub[d] = ub[d];
+      }
+    } else if (op.name == "func.return") {
+    } else {
+      throw std::runtime_error("unsupported op in a multi-apply step: " + op.name);
+    }
+  }
+  p.nops = static_cast<int>(c.ops.size());
+  p.ops = c.ops.data();
+  p.napplies = static_cast<int>(c.applies.size());
+  p.applies = c.applies.data();
+  timeSlotsInto(module, p);
+  if (c.decomposed && p.nstores > 0)
+    for (int d = 0; d < p.rank; ++d)
+      c.decomp.core[d] = p.mstore[0].ub[d] - p.mstore[0].lb[d];
+  return c;
 }
 
 // Throws std::runtime_error with a reason when the module is outside the descriptor's reach.
@@ -89,6 +242,20 @@ inline Converted convert(const halogen::ir::Operation &module) {
   std::map<const Value *, int> loadOf;   // stencil.load result -> field arg
   std::map<const Value *, int> applyRes; // apply result -> result index
   int napply = 0;
+  // multi-apply form when there are several applies or one consumes another
+  {
+    int n = 0;
+    bool chained = false;
+    for (const auto &opPtr : body.ops)
+      if (opPtr->name == "stencil.apply") {
+        ++n;
+        for (const Value *o : opPtr->operands)
+          if (o->defOp && o->defOp->name == "stencil.apply")
+            chained = true;
+      }
+    if (n > 1 || chained)
+      return convertMulti(module, entry, std::move(c));
+  }
   for (const auto &opPtr : body.ops) {
     const Operation &op = *opPtr;
     if (op.name == "stencil.load") {
@@ -96,27 +263,7 @@ inline Converted convert(const halogen::ir::Operation &module) {
         throw std::runtime_error("stencil.load of a non-argument");
       loadOf[&op.results[0]] = op.operands[0]->argIdx;
     } else if (op.name == "dmp.swap") {
-      c.decomposed = true;
-      if (c.decomp.nswaps >= HG_MAX_FIELDS)
-        throw std::runtime_error("too many swaps");
-      hg_swap &s = c.decomp.swaps[c.decomp.nswaps++];
-      s.field = op.operands[0]->argIdx;
-      const auto *g = op.attr("grid")->dynAs<GridAttr>();
-      c.decomp.ndim = static_cast<int>(g->dims.size());
-      for (int d = 0; d < c.decomp.ndim; ++d)
-        c.decomp.grid[d] = g->dims[static_cast<std::size_t>(d)];
-      const auto *xs = op.attr("exchanges")->dynAs<ArrayAttr>();
-      s.nexchanges = 0;
-      for (const Attribute &a : xs->elems) {
-        const auto &e = a.as<ExchangeAttr>();
-        hg_exchange &x = s.ex[s.nexchanges++];
-        for (std::size_t d = 0; d < e.at.size(); ++d) {
-          x.at[d] = e.at[d];
-          x.size[d] = e.size[d];
-          x.offset[d] = e.offset[d];
-          x.to[d] = e.to[d];
-        }
-      }
+      swapInto(op, c);
     } else if (op.name == "stencil.apply") {
       if (++napply > 1)
         throw std::runtime_error("more than one stencil.apply per step");
@@ -185,17 +332,7 @@ inline Converted convert(const halogen::ir::Operation &module) {
   }
   p.nops = static_cast<int>(c.ops.size());
   p.ops = c.ops.data();
-  if (const Attribute *ts = module.attr("stencil.time_slots")) {
-    const auto &outer = ts->as<ArrayAttr>();
-    int at = 0;
-    for (const Attribute &g : outer.elems) {
-      std::vector<std::int64_t> idx;
-      attrToIndexVector(g, idx);
-      p.group_len[p.ngroups++] = static_cast<int>(idx.size());
-      for (auto i : idx)
-        p.groups[at++] = static_cast<int>(i);
-    }
-  }
+  timeSlotsInto(module, p);
   if (c.decomposed) {
     // per-rank core = the (rank-0) store region written by decompose (dmp_transforms.cpp:262-272)
     for (int d = 0; d < p.rank; ++d)

@@ -112,7 +112,11 @@ void or_binding_after(int ngroups, const int32_t *glen, const int32_t *groups, i
  * result buffers (:713-758) with bounds-checked accesses (:759-780), then each
  * stencil.store copies its region (:683-712).  Results are staged so an in-place store
  * sees the loaded (pre-step) values, as the clone does. */
+static int or_step_multi(const hg_program *p, or_buf **slots, int nthreads);
+
 int or_step(const hg_program *p, or_buf **slots, int nthreads) {
+  if (p->napplies > 0)
+    return or_step_multi(p, slots, nthreads);
   int r = p->rank;
   /* apply domain = hull of the store regions (propagate-bounds' result bounds) */
   int64_t ia[3] = {0, 0, 0}, ib[3] = {1, 1, 1};
@@ -457,8 +461,9 @@ static int sim_core(const hg_program *local, const hg_decomp *dc, or_buf **globa
     return fail("process grid rank does not match the domain");
   /* rank-0 core lower bound = the local store region's lb */
   int64_t core_lb[3] = {0, 0, 0};
+  const hg_bounds *st0 = local->napplies > 0 ? &local->mstore[0] : &local->store[0];
   for (int d = 0; d < r; ++d)
-    core_lb[d] = local->store[0].lb[d];
+    core_lb[d] = st0->lb[d];
   or_buf ***rb = (or_buf ***)calloc((size_t)P, sizeof(or_buf **));
   for (int64_t q = 0; q < P; ++q) {
     rb[q] = (or_buf **)calloc((size_t)nfields, sizeof(or_buf *));
@@ -571,4 +576,118 @@ int or_simulate_rank_state(const hg_program *local, const hg_decomp *dc, or_buf 
                            int nfields, int64_t T, int64_t want_rank, or_buf **local_out,
                            int nthreads) {
   return sim_core(local, dc, global_init, nfields, T, NULL, want_rank, local_out, nthreads);
+}
+
+/* Multi-apply step: applies run in program order; each evaluates its region over its whole
+ * result bounds into fresh temps (materializeApply, stencil_transforms.cpp:334-379; the
+ * interpreter does the same per apply, interpreter.cpp:713-758); field operands read the
+ * loaded (pre-step) values; then every stencil.store copies its region (:683-712). */
+static int or_step_multi(const hg_program *p, or_buf **slots, int nthreads) {
+  const int r = p->rank, es = p->dtype == HG_F32 ? 4 : 8;
+  or_buf tmp[HG_MAX_TEMPS];
+  memset(tmp, 0, sizeof tmp);
+  int rc = 0;
+  (void)nthreads;
+  for (int a = 0; a < p->napplies && !rc; ++a) {
+    const hg_apply *A = &p->applies[a];
+    const hg_op *ops = p->ops + A->op_begin;
+    int64_t ext[3] = {1, 1, 1}, npts = 1;
+    for (int d = 0; d < r; ++d) {
+      ext[d] = A->domain.ub[d] - A->domain.lb[d];
+      npts *= ext[d];
+    }
+    for (int k = 0; k < A->nresults; ++k) {
+      or_buf *t = &tmp[A->result_temp[k]];
+      t->rank = r;
+      t->elem = es;
+      for (int d = 0; d < r; ++d) {
+        t->lb[d] = A->domain.lb[d];
+        t->shape[d] = ext[d];
+      }
+      t->data = (unsigned char *)calloc((size_t)npts, (size_t)es);
+    }
+    const or_buf *opb[HG_MAX_FIELDS];
+    for (int o = 0; o < A->noperands; ++o)
+      opb[o] = A->operand[o] >= 0 ? slots[A->operand[o]] : &tmp[-A->operand[o] - 1];
+    int trapped = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < npts; ++q) {
+      float vf[1024];
+      double vd[1024];
+      int64_t pt[3], rem = q;
+      for (int d = r - 1; d >= 0; --d) {
+        pt[d] = A->domain.lb[d] + rem % ext[d];
+        rem /= ext[d];
+      }
+      for (int i = 0; i < A->nops && i < 1024; ++i) {
+        const hg_op *op = &ops[i];
+        switch (op->code) {
+        case HG_OP_ACCESS: {
+          const or_buf *b = opb[op->operand];
+          int64_t idx = 0;
+          for (int d = 0; d < r; ++d) {
+            int64_t rr = pt[d] + op->off[d] - b->lb[d];
+            if (rr < 0 || rr >= b->shape[d]) {
+              trapped = 1;
+              rr = 0;
+            }
+            idx = idx * b->shape[d] + rr;
+          }
+          if (es == 4) memcpy(&vf[i], b->data + idx * 4, 4); else memcpy(&vd[i], b->data + idx * 8, 8);
+          break;
+        }
+        case HG_OP_CONST:
+          if (es == 4) {
+            uint32_t u = (uint32_t)op->bits;
+            memcpy(&vf[i], &u, 4);
+          } else {
+            memcpy(&vd[i], &op->bits, 8);
+          }
+          break;
+        case HG_OP_ADD: if (es == 4) vf[i] = vf[op->a] + vf[op->b]; else vd[i] = vd[op->a] + vd[op->b]; break;
+        case HG_OP_SUB: if (es == 4) vf[i] = vf[op->a] - vf[op->b]; else vd[i] = vd[op->a] - vd[op->b]; break;
+        case HG_OP_MUL: if (es == 4) vf[i] = vf[op->a] * vf[op->b]; else vd[i] = vd[op->a] * vd[op->b]; break;
+        default: if (es == 4) vf[i] = vf[op->a] / vf[op->b]; else vd[i] = vd[op->a] / vd[op->b]; break;
+        }
+      }
+      for (int k = 0; k < A->nresults; ++k) {
+        or_buf *t = &tmp[A->result_temp[k]];
+        if (es == 4) memcpy(t->data + q * 4, &vf[A->result_op[k]], 4);
+        else memcpy(t->data + q * 8, &vd[A->result_op[k]], 8);
+      }
+    }
+    if (trapped)
+      rc = fail("stencil access escapes the value bounds");
+  }
+  for (int k = 0; k < p->nstores && !rc; ++k) {
+    const or_buf *src = &tmp[p->mstore_temp[k]];
+    or_buf *dst = slots[p->mstore_field[k]];
+    const hg_bounds *sb = &p->mstore[k];
+    int64_t se[3] = {1, 1, 1}, sn = 1;
+    for (int d = 0; d < r; ++d) {
+      se[d] = sb->ub[d] - sb->lb[d];
+      sn *= se[d];
+    }
+    for (int64_t q = 0; q < sn && !rc; ++q) {
+      int64_t rem = q, pt[3], si = 0, di = 0;
+      for (int d = r - 1; d >= 0; --d) {
+        pt[d] = sb->lb[d] + rem % se[d];
+        rem /= se[d];
+      }
+      for (int d = 0; d < r; ++d) {
+        int64_t sr = pt[d] - src->lb[d], dr = pt[d] - dst->lb[d];
+        if (sr < 0 || sr >= src->shape[d] || dr < 0 || dr >= dst->shape[d]) {
+          rc = fail("store region escapes the field bounds");
+          break;
+        }
+        si = si * src->shape[d] + sr;
+        di = di * dst->shape[d] + dr;
+      }
+      if (!rc)
+        memcpy(dst->data + di * es, src->data + si * es, (size_t)es);
+    }
+  }
+  for (int t = 0; t < HG_MAX_TEMPS; ++t)
+    free(tmp[t].data);
+  return rc;
 }

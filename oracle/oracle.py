@@ -194,7 +194,8 @@ class Ref:
                                         P(C.c_int)]),
             ("hr_laplacian_weight", C.c_double, [C.c_int, LL]),
             ("hr_export_program", C.c_int, [V, P(capi.HgProgram), P(capi.HgOp), C.c_int,
-                                            P(capi.HgDecomp), P(C.c_int)]),
+                                            P(capi.HgDecomp), P(C.c_int), P(capi.HgApply),
+                                            C.c_int]),
         ]:
             f = getattr(L, name)
             f.restype = res
@@ -244,10 +245,12 @@ class Ref:
     def export_program(self, mod):
         prog = capi.HgProgram()
         ops = (capi.HgOp * capi.HG_MAX_OPS)()
+        applies = (capi.HgApply * capi.HG_MAX_APPLIES)()
         dc = capi.HgDecomp()
         dec = C.c_int()
         n = self.L.hr_export_program(mod, C.byref(prog), ops, capi.HG_MAX_OPS, C.byref(dc),
-                                     C.byref(dec))
+                                     C.byref(dec), applies, capi.HG_MAX_APPLIES)
         if n < 0:
             raise RuntimeError(self.err())
+        prog._applies_keepalive = applies
         return prog, ops, (dc if dec.value else None)

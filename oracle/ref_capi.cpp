@@ -278,16 +278,20 @@ double hr_laplacian_weight(int order, long long k) { return exec::laplacianWeigh
 // The reference module read into the hg descriptor (integration/ir_to_hg.hpp); ops are copied
 // into ops[cap].  Returns the op count, or -1 with hr_last_error set.
 int hr_export_program(void *mod, hg_program *out, hg_op *ops, int cap, hg_decomp *dc,
-                      int *decomposed) {
+                      int *decomposed, hg_apply *applies, int cap_applies) {
   try {
     auto c = hg_ir::convert(*static_cast<Mod *>(mod)->m);
-    if (static_cast<int>(c.ops.size()) > cap) {
-      g_err = "op buffer too small";
+    if (static_cast<int>(c.ops.size()) > cap ||
+        static_cast<int>(c.applies.size()) > cap_applies) {
+      g_err = "op/apply buffer too small";
       return -1;
     }
     std::memcpy(ops, c.ops.data(), c.ops.size() * sizeof(hg_op));
+    if (!c.applies.empty())
+      std::memcpy(applies, c.applies.data(), c.applies.size() * sizeof(hg_apply));
     *out = c.prog;
     out->ops = ops;
+    out->applies = c.applies.empty() ? nullptr : applies;
     if (dc)
       *dc = c.decomp;
     if (decomposed)

@@ -136,6 +136,7 @@ class Program:
     def __init__(self, prog: HgProgram, ops):
         self.prog = prog
         self.ops = ops
+        self.applies = None
         self.prog.ops = C.cast(self.ops, C.POINTER(HgOp))
 
     @staticmethod
@@ -148,15 +149,47 @@ class Program:
         for i, (lb, ub) in enumerate(j["fields"]):
             for d in range(r):
                 p.fields[i].lb[d], p.fields[i].ub[d] = lb[d], ub[d]
-        p.noperands = len(j["operand_field"])
-        for i, f in enumerate(j["operand_field"]):
+        loads = j["loads"] if "applies" in j else j["operand_field"]
+        for i, f in enumerate(loads):
             p.operand_field[i] = f
+        p.noperands = len(loads)
         for i, (code, a, b, operand, off, bits) in enumerate(j["ops"]):
             ops[i].code, ops[i].a, ops[i].b, ops[i].operand = code, a, b, operand
             for d in range(r):
                 ops[i].off[d] = off[d]
             ops[i].bits = int(bits, 16)
         p.nops = len(j["ops"])
+        if "applies" in j:  # multi-apply step
+            aps = (capi.HgApply * max(len(j["applies"]), 1))()
+            for a, A in enumerate(j["applies"]):
+                aps[a].noperands = len(A["operands"])
+                for o, x in enumerate(A["operands"]):
+                    aps[a].operand[o] = x
+                aps[a].op_begin, aps[a].nops = A["op_begin"], A["nops"]
+                aps[a].nresults = len(A["result_op"])
+                for k in range(aps[a].nresults):
+                    aps[a].result_op[k] = A["result_op"][k]
+                    aps[a].result_temp[k] = A["result_temp"][k]
+                for d in range(r):
+                    aps[a].domain.lb[d], aps[a].domain.ub[d] = A["domain"][0][d], A["domain"][1][d]
+            p.napplies = len(j["applies"])
+            p.ntemps = j["ntemps"]
+            p.nstores = len(j["mstores"])
+            for k, (t, f, lb, ub) in enumerate(j["mstores"]):
+                p.mstore_temp[k], p.mstore_field[k] = t, f
+                for d in range(r):
+                    p.mstore[k].lb[d], p.mstore[k].ub[d] = lb[d], ub[d]
+            p.ngroups = len(j["groups"])
+            at = 0
+            for g, grp in enumerate(j["groups"]):
+                p.group_len[g] = len(grp)
+                for x in grp:
+                    p.groups[at] = x
+                    at += 1
+            prog = Program(p, ops)
+            prog.applies = aps
+            prog.prog.applies = C.cast(aps, C.POINTER(capi.HgApply))
+            return prog
         p.nresults = len(j["result_op"])
         for k in range(p.nresults):
             p.result_op[k], p.store_field[k] = j["result_op"][k], j["store_field"][k]
@@ -177,13 +210,19 @@ class Program:
         """Read `.xir` text (hg_parse_program).  Returns (Program, HgDecomp or None,
         dmp.reference text)."""
         ops = (HgOp * capi.HG_MAX_OPS)()
+        aps = (capi.HgApply * capi.HG_MAX_APPLIES)()
         prog = HgProgram()
         dc = HgDecomp()
         dec = C.c_int()
         ref = C.create_string_buffer(1 << 20)
-        check(lib().hg_parse_program(text.encode(), C.byref(prog), ops, capi.HG_MAX_OPS,
-                                     C.byref(dc), C.byref(dec), ref, 1 << 20))
-        return Program(prog, ops), (dc if dec.value else None), ref.value.decode()
+        check(lib().hg_parse_program(text.encode(), C.byref(prog), ops, capi.HG_MAX_OPS, aps,
+                                     capi.HG_MAX_APPLIES, C.byref(dc), C.byref(dec), ref,
+                                     1 << 20))
+        out = Program(prog, ops)
+        if prog.napplies > 0:
+            out.applies = aps
+            out.prog.applies = C.cast(aps, C.POINTER(capi.HgApply))
+        return out, (dc if dec.value else None), ref.value.decode()
 
     @staticmethod
     def pw_advection(nz: int, ny: int, nx: int) -> "Program":
@@ -229,8 +268,12 @@ class Program:
             at += n
         return out
 
+    def store_region(self, k: int = 0):
+        """Stored region k (hg_bounds) of either program form."""
+        return self.prog.mstore[k] if self.prog.napplies > 0 else self.prog.store[k]
+
     def core_points(self) -> int:
-        s = self.prog.store[0]
+        s = self.store_region(0)
         n = 1
         for d in range(self.rank):
             n *= s.ub[d] - s.lb[d]
@@ -245,9 +288,16 @@ class Program:
         """The decompose pass: returns (local program, HgDecomp)."""
         local = HgProgram()
         dc = HgDecomp()
+        aps = None
+        if self.prog.napplies > 0:
+            aps = (capi.HgApply * self.prog.napplies)()
+            local.applies = C.cast(aps, C.POINTER(capi.HgApply))
         check(lib().hg_decompose_program(C.byref(self.prog), len(grid), _i64(grid),
                                          C.byref(local), C.byref(dc)))
-        return Program(local, self.ops), dc
+        out = Program(local, self.ops)
+        if aps is not None:
+            out.applies = aps
+        return out, dc
 
     def with_extents(self, extents: Sequence[int]) -> "Program":
         """The same step program over a non-cubic domain [0, extents) (buildKernel is cubic,
@@ -466,10 +516,10 @@ def simulate(prog: Program, grid: Sequence[int], global_init: List[Buffer], time
                 loc = plans[r].download(perm[i])
                 llo, _ = local.field_bounds(perm[i])
                 g = out[i]
-                src = tuple(slice(local.prog.store[0].lb[d] - llo[d],
-                                  local.prog.store[0].ub[d] - llo[d]) for d in range(prog.rank))
-                dst = tuple(slice(local.prog.store[0].lb[d] + coord[d] * dc.core[d] - g.lb[d],
-                                  local.prog.store[0].ub[d] + coord[d] * dc.core[d] - g.lb[d])
+                sr = local.store_region(0)
+                src = tuple(slice(sr.lb[d] - llo[d], sr.ub[d] - llo[d]) for d in range(prog.rank))
+                dst = tuple(slice(sr.lb[d] + coord[d] * dc.core[d] - g.lb[d],
+                                  sr.ub[d] + coord[d] * dc.core[d] - g.lb[d])
                             for d in range(prog.rank))
                 g.data[dst] = loc[src]
         return out

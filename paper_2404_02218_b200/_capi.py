@@ -13,6 +13,9 @@ HG_MAX_RANK = 3
 HG_MAX_FIELDS = 16
 HG_MAX_RESULTS = 8
 HG_MAX_OPS = 4096
+HG_MAX_APPLIES = 32
+HG_MAX_TEMPS = 64
+HG_MAX_STORES = 16
 
 HG_OK, HG_EINVAL, HG_EUNSUPPORTED, HG_ECUDA, HG_ETRAP, HG_ENOMEM, HG_ESTATE = range(7)
 HG_F32, HG_F64 = 1, 2
@@ -30,6 +33,13 @@ class HgBounds(C.Structure):
     _fields_ = [("lb", i64x3), ("ub", i64x3)]
 
 
+class HgApply(C.Structure):
+    _fields_ = [("noperands", C.c_int32), ("operand", C.c_int32 * HG_MAX_FIELDS),
+                ("op_begin", C.c_int32), ("nops", C.c_int32), ("nresults", C.c_int32),
+                ("result_op", C.c_int32 * HG_MAX_RESULTS),
+                ("result_temp", C.c_int32 * HG_MAX_RESULTS), ("domain", HgBounds)]
+
+
 class HgProgram(C.Structure):
     _fields_ = [
         ("rank", C.c_int32), ("dtype", C.c_int32), ("nfields", C.c_int32),
@@ -40,6 +50,9 @@ class HgProgram(C.Structure):
         ("store_field", C.c_int32 * HG_MAX_RESULTS), ("store", HgBounds * HG_MAX_RESULTS),
         ("ngroups", C.c_int32), ("group_len", C.c_int32 * HG_MAX_FIELDS),
         ("groups", C.c_int32 * HG_MAX_FIELDS),
+        ("napplies", C.c_int32), ("applies", C.POINTER(HgApply)), ("ntemps", C.c_int32),
+        ("nstores", C.c_int32), ("mstore_temp", C.c_int32 * HG_MAX_STORES),
+        ("mstore_field", C.c_int32 * HG_MAX_STORES), ("mstore", HgBounds * HG_MAX_STORES),
     ]
 
 
@@ -102,8 +115,8 @@ def lib() -> C.CDLL:
                                               P(HgProgram), P(HgOp), C.c_int]),
         "hg_program_match": (C.c_int, [P(HgProgram), C.c_char_p, SZ]),
         "hg_apply_compile": (C.c_int, [P(HgProgram), C.c_char_p, SZ, P(SZ)]),
-        "hg_parse_program": (C.c_int, [C.c_char_p, P(HgProgram), P(HgOp), C.c_int, P(HgDecomp),
-                                       P(C.c_int), C.c_char_p, SZ]),
+        "hg_parse_program": (C.c_int, [C.c_char_p, P(HgProgram), P(HgOp), C.c_int, P(HgApply),
+                                       C.c_int, P(HgDecomp), P(C.c_int), C.c_char_p, SZ]),
         "hg_decompose_program": (C.c_int, [P(HgProgram), C.c_int, P(I64), P(HgProgram),
                                            P(HgDecomp)]),
         "hg_plan_create": (C.c_int, [P(HgProgram), C.c_int, P(V)]),

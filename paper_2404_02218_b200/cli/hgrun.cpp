@@ -51,6 +51,7 @@ std::string readAll(const std::string &path) {
 struct Prog {
   hg_program p{};
   std::vector<hg_op> ops = std::vector<hg_op>(HG_MAX_OPS);
+  std::vector<hg_apply> applies = std::vector<hg_apply>(HG_MAX_APPLIES);
   hg_decomp dc{};
   int decomposed = 0;
   std::string reference;
@@ -59,11 +60,13 @@ struct Prog {
 Prog parse(const std::string &text) {
   Prog P;
   std::vector<char> ref(1 << 22);
-  ok(hg_parse_program(text.c_str(), &P.p, P.ops.data(), HG_MAX_OPS, &P.dc, &P.decomposed,
-                      ref.data(), ref.size()),
+  ok(hg_parse_program(text.c_str(), &P.p, P.ops.data(), HG_MAX_OPS, P.applies.data(),
+                      HG_MAX_APPLIES, &P.dc, &P.decomposed, ref.data(), ref.size()),
      "parse");
   P.reference = ref.data();
   P.p.ops = P.ops.data();
+  if (P.p.napplies > 0)
+    P.p.applies = P.applies.data();
   return P;
 }
 
@@ -164,7 +167,7 @@ std::vector<std::vector<unsigned char>> simulate(const hg_program &global, const
       std::vector<unsigned char> l(static_cast<size_t>(count(local.fields[b], r)) * es);
       ok(hg_plan_download(plans[static_cast<size_t>(q)], b, l.data(), l.size(), nullptr), "dl");
       const hg_bounds &lb = local.fields[b], &gb = global.fields[b];
-      const hg_bounds &core = local.store[0];
+      const hg_bounds &core = local.napplies > 0 ? local.mstore[0] : local.store[0];
       int64_t n = count(core, r);
       for (int64_t k = 0; k < n; ++k) { // gatherRank (simulator.cpp:1027-1060)
         int64_t rem = k, p[3] = {0, 0, 0};

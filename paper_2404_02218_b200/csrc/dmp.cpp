@@ -361,10 +361,14 @@ int hg_dmp_run(hg_dmp *d, int64_t steps, void *stream) {
     }
     // 3. fuse the NEXT step's swap of the output into this kernel (not on the last step of
     //    the call: the reference swaps a buffer only right before it is loaded)
-    const int bOut = p.bind[static_cast<size_t>(g.store_field[0])];
+    // the buffers this step writes (bindings before the step rotates them)
+    std::vector<int> written;
+    for (int k = 0; k < storedCount(g); ++k)
+      written.push_back(p.bind[static_cast<size_t>(storedField(g, k))]);
+    const int bOut = written[0];
     int nextSlot = -1; // the argument slot the output buffer occupies next step
     for (size_t i = 0; i < p.an.src.size(); ++i)
-      if (p.an.src[i] == g.store_field[0])
+      if (p.an.src[i] == storedField(g, 0))
         nextSlot = static_cast<int>(i);
     const hg_swap *sw = nullptr;
     for (int k = 0; k < d->dc.nswaps && nextSlot >= 0; ++k)
@@ -431,13 +435,9 @@ int hg_dmp_run(hg_dmp *d, int64_t steps, void *stream) {
     if (rc)
       return rc;
     mark();
+    for (size_t k = 1; k < written.size(); ++k) // (multi-store programs never fuse)
+      d->dirty[static_cast<size_t>(written[k])] = 1;
     d->dirty[static_cast<size_t>(bOut)] = fused ? 0 : 1;
-    for (int k = 1; k < g.nresults; ++k) { // (multi-result programs never fuse)
-      std::vector<int> prevBind(p.bind.size());
-      for (size_t i = 0; i < p.bind.size(); ++i)
-        prevBind[static_cast<size_t>(p.an.src[i])] = p.bind[i];
-      d->dirty[static_cast<size_t>(prevBind[static_cast<size_t>(g.store_field[k])])] = 1;
-    }
     if (fused)
       ++d->epoch;
     roundReady = fused;
@@ -544,15 +544,15 @@ int hg_sim_run(hg_dmp **ranks, int n, int64_t steps, void **streams) {
           if (rc)
             return rc;
         }
+      const hg_program &g = p.prog;
+      std::vector<int> written;
+      for (int k = 0; k < storedCount(g); ++k)
+        written.push_back(p.bind[static_cast<size_t>(storedField(g, k))]);
       rc = planStep(p, st);
       if (rc)
         return rc;
-      const hg_program &g = p.prog;
-      std::vector<int> prevBind(p.bind.size());
-      for (size_t k = 0; k < p.bind.size(); ++k)
-        prevBind[static_cast<size_t>(p.an.src[k])] = p.bind[k];
-      for (int k = 0; k < g.nresults; ++k)
-        d.dirty[static_cast<size_t>(prevBind[static_cast<size_t>(g.store_field[k])])] = 1;
+      for (int b : written)
+        d.dirty[static_cast<size_t>(b)] = 1;
     }
   }
   return HG_OK;

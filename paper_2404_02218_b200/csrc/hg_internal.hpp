@@ -14,7 +14,7 @@ namespace hg {
 int setError(int status, const std::string &msg);
 
 // ---- program analysis (program.cpp) ----------------------------------------------------
-enum class Family { Generic = 0, Star = 1, Apply = 2 };
+enum class Family { Generic = 0, Star = 1, Apply = 2, Multi = 3 };
 enum StarKind { kHeat = 0, kWave = 1, kCopy = 2 };
 
 // The star-Laplacian family the generator emits (kernels.cpp:110-135, 205-226):
@@ -43,6 +43,15 @@ struct Analysis {
 // Validates + classifies.  Returns HG_OK or an error status (message set).
 int analyze(const hg_program &p, Analysis &out);
 int validateProgram(const hg_program &p);
+
+// the stores of either program form (single apply: one per result; multi-apply: nstores)
+inline int storedCount(const hg_program &g) { return g.napplies > 0 ? g.nstores : g.nresults; }
+inline int storedField(const hg_program &g, int k) {
+  return g.napplies > 0 ? g.mstore_field[k] : g.store_field[k];
+}
+inline const hg_bounds &storedRegion(const hg_program &g, int k) {
+  return g.napplies > 0 ? g.mstore[k] : g.store[k];
+}
 
 // ---- device layout -----------------------------------------------------------------------
 struct Layout {

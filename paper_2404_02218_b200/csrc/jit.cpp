@@ -117,6 +117,8 @@ bool jitEligible(const hg_program &p, const Analysis &a, std::string *why) {
   };
   if (p.rank < 2)
     return no("rank 1");
+  if (p.napplies > 0)
+    return no("multi-apply step");
   for (int f = 1; f < p.nfields; ++f)
     for (int d = 0; d < p.rank; ++d)
       if (p.fields[f].lb[d] != p.fields[0].lb[d] || p.fields[f].ub[d] != p.fields[0].ub[d])

@@ -39,6 +39,15 @@
 #ifndef HG_TYT_R4
 #define HG_TYT_R4 16
 #endif
+#ifndef HG_TXT_R4
+#define HG_TXT_R4 16
+#endif
+#ifndef HG_TYT_R2
+#define HG_TYT_R2 16
+#endif
+#ifndef HG_TXT_R2
+#define HG_TXT_R2 16
+#endif
 
 namespace hg {
 
@@ -159,7 +168,8 @@ __device__ __forceinline__ void st4(double *p, const V4<double> &v) {
 // taller (more consumer warps in the single CTA an SM holds at ~110 registers).
 template <int RANK, int R> struct StarGeom;
 template <int R> struct StarGeom<3, R> {
-  static constexpr int TXT = 16, TYT = R >= 4 ? HG_TYT_R4 : 16;
+  static constexpr int TXT = R >= 4 ? HG_TXT_R4 : HG_TXT_R2;
+  static constexpr int TYT = R >= 4 ? HG_TYT_R4 : HG_TYT_R2;
 };
 template <int R> struct StarGeom<2, R> {
   static constexpr int TXT = 32, TYT = 1;
@@ -802,6 +812,20 @@ template <typename T> __global__ void genericKernel(const __grid_constant__ GenP
   }
 }
 
+// ---- stencil.store between two layouts (multi-apply temps -> fields) -----------------------
+template <typename T>
+__global__ void copyBoxKernel(const T *src, const DevLayout SL, T *dst, const DevLayout DL,
+                              int64_t l0, int64_t l1, int64_t l2, int64_t e0, int64_t e1,
+                              int64_t e2) {
+  const int64_t total = e0 * e1 * e2;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    int64_t p[3] = {l0 + k / (e1 * e2), l1 + (k / e2) % e1, l2 + k % e2};
+    // rank < 3 uses the leading entries only
+    dst[layIndex(DL, p)] = src[layIndex(SL, p)];
+  }
+}
+
 // ---- initializer: exec::fillInit / initValue (buffer.cpp:142-179) ---------------------------
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ull;
@@ -982,7 +1006,8 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = dtype == HG_F32 ? 4 : 8;
   const int R = s.radius;
-  const int TX = (rank == 3 ? StarGeom<3, 1>::TXT : StarGeom<2, 1>::TXT) * 4;
+  const int TX = (rank == 3 ? (R >= 4 ? StarGeom<3, 4>::TXT : StarGeom<3, 1>::TXT)
+                            : StarGeom<2, 1>::TXT) * 4;
   const int TY = rank == 3 ? (R >= 4 ? StarGeom<3, 4>::TYT : StarGeom<3, 1>::TYT) : 1;
   const int RY = rank == 3 ? R : 0;
   cuuint64_t dims[3], strides[2];
@@ -1095,6 +1120,29 @@ int launchInit(void *base, const DevLayout &lay, int field, const int64_t *origi
     initKernel<double><<<blocks, 256, 0, st>>>(static_cast<double *>(base), lay, seed, o0, o1,
                                                o2, total);
   return cudaErr(cudaGetLastError(), "init kernel launch");
+}
+
+int launchCopyBox(const void *src, const DevLayout &sl, void *dst, const DevLayout &dl,
+                  const int64_t *lb, const int64_t *ub, cudaStream_t st) {
+  int64_t l[3] = {0, 0, 0}, e[3] = {1, 1, 1};
+  for (int d = 0; d < sl.rank; ++d) {
+    l[d] = lb[d];
+    e[d] = ub[d] - lb[d];
+  }
+  const int64_t total = e[0] * e[1] * e[2];
+  if (total <= 0)
+    return HG_OK;
+  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256,
+                                                                          148 * 16)));
+  if (sl.es == 4)
+    copyBoxKernel<float><<<blocks, 256, 0, st>>>(static_cast<const float *>(src), sl,
+                                                 static_cast<float *>(dst), dl, l[0], l[1], l[2],
+                                                 e[0], e[1], e[2]);
+  else
+    copyBoxKernel<double><<<blocks, 256, 0, st>>>(static_cast<const double *>(src), sl,
+                                                  static_cast<double *>(dst), dl, l[0], l[1],
+                                                  l[2], e[0], e[1], e[2]);
+  return cudaErr(cudaGetLastError(), "copy kernel launch");
 }
 
 int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,

@@ -72,6 +72,9 @@ int launchGeneric(const GenericLaunch &L, cudaStream_t st);
 // ---- fields -----------------------------------------------------------------------------
 int launchInit(void *base, const DevLayout &lay, int field, const int64_t *origin,
                cudaStream_t st);
+// stencil.store between layouts: dst[p] = src[p] for logical points p in [lb, ub)
+int launchCopyBox(const void *src, const DevLayout &sl, void *dst, const DevLayout &dl,
+                  const int64_t *lb, const int64_t *ub, cudaStream_t st);
 // box copy between a layout box and a packed array (dir 0 = pack, 1 = unpack)
 int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,
                      void *packed, int unpack, cudaStream_t st);

@@ -38,24 +38,27 @@ std::shared_ptr<JitKernel> jitCached(const hg_program &g, int device) {
 }
 
 // Linear-scan slot allocation for the generic kernel: a value lives until its last use.
-int compileGeneric(hg_plan &p) {
-  const hg_program &g = p.prog;
-  std::vector<int> last(static_cast<size_t>(g.nops), -1);
-  for (int i = 0; i < g.nops; ++i) {
-    const hg_op &o = g.ops[i];
+// Compiles one apply region (ops[0..nops), region-relative operand indices) whose operand o
+// is laid out as lay[o].
+int compileSlice(int rank, const hg_op *ops, int nops, const int32_t *resultOp, int nresults,
+                 const std::vector<const Layout *> &lay, std::vector<GOp> &out, int &nslots,
+                 std::vector<int> &resSlot) {
+  std::vector<int> last(static_cast<size_t>(nops), -1);
+  for (int i = 0; i < nops; ++i) {
+    const hg_op &o = ops[i];
     if (o.code >= HG_OP_ADD) {
       last[static_cast<size_t>(o.a)] = std::max(last[static_cast<size_t>(o.a)], i);
       last[static_cast<size_t>(o.b)] = std::max(last[static_cast<size_t>(o.b)], i);
     }
   }
-  for (int k = 0; k < g.nresults; ++k)
-    last[static_cast<size_t>(g.result_op[k])] = g.nops;
-  std::vector<int> slot(static_cast<size_t>(g.nops), -1);
+  for (int k = 0; k < nresults; ++k)
+    last[static_cast<size_t>(resultOp[k])] = nops;
+  std::vector<int> slot(static_cast<size_t>(nops), -1);
   std::vector<int> freeSlots;
-  int nslots = 0;
-  std::vector<GOp> out(static_cast<size_t>(g.nops));
-  for (int i = 0; i < g.nops; ++i) {
-    const hg_op &o = g.ops[i];
+  nslots = 0;
+  out.assign(static_cast<size_t>(nops), GOp{});
+  for (int i = 0; i < nops; ++i) {
+    const hg_op &o = ops[i];
     GOp &q = out[static_cast<size_t>(i)];
     std::memset(&q, 0, sizeof q);
     q.code = o.code;
@@ -83,27 +86,141 @@ int compileGeneric(hg_plan &p) {
       freeSlots.push_back(s);
     if (o.code == HG_OP_ACCESS) {
       q.operand = static_cast<int16_t>(o.operand);
-      const Layout &L = p.lay[static_cast<size_t>(g.operand_field[o.operand])];
+      const Layout &L = *lay[static_cast<size_t>(o.operand)];
       int64_t stride = 1, delta = 0;
-      for (int d = g.rank - 1; d >= 0; --d) {
+      for (int d = rank - 1; d >= 0; --d) {
         delta += o.off[d] * stride;
-        stride *= d == g.rank - 1 ? L.pitch : L.shape[d];
+        stride *= d == rank - 1 ? L.pitch : L.shape[d];
       }
       q.delta = delta;
     } else if (o.code == HG_OP_CONST) {
       q.bits = o.bits;
     }
   }
-  p.nslots = nslots;
-  p.resSlot.clear();
-  for (int k = 0; k < g.nresults; ++k)
-    p.resSlot.push_back(slot[static_cast<size_t>(g.result_op[k])]);
-  int st = cudaCheck(cudaMalloc(&p.gopsDev, sizeof(GOp) * out.size()), "cudaMalloc(ops)");
+  resSlot.clear();
+  for (int k = 0; k < nresults; ++k)
+    resSlot.push_back(slot[static_cast<size_t>(resultOp[k])]);
+  if (nslots > 48)
+    return setError(HG_EUNSUPPORTED, "apply region needs too many live values");
+  return HG_OK;
+}
+
+int uploadOps(const std::vector<GOp> &ops, GOp **dev) {
+  int st = cudaCheck(cudaMalloc(dev, sizeof(GOp) * std::max<size_t>(ops.size(), 1)),
+                     "cudaMalloc(ops)");
   if (st)
     return st;
-  return cudaCheck(cudaMemcpy(p.gopsDev, out.data(), sizeof(GOp) * out.size(),
-                              cudaMemcpyHostToDevice),
+  return cudaCheck(cudaMemcpy(*dev, ops.data(), sizeof(GOp) * ops.size(), cudaMemcpyHostToDevice),
                    "cudaMemcpy(ops)");
+}
+
+int compileGeneric(hg_plan &p) {
+  const hg_program &g = p.prog;
+  std::vector<const Layout *> lay;
+  for (int o = 0; o < g.noperands; ++o)
+    lay.push_back(&p.lay[static_cast<size_t>(g.operand_field[o])]);
+  std::vector<GOp> out;
+  int st = compileSlice(g.rank, g.ops, g.nops, g.result_op, g.nresults, lay, out, p.nslots,
+                        p.resSlot);
+  if (st)
+    return st;
+  return uploadOps(out, &p.gopsDev);
+}
+
+// Multi-apply: one compiled slice per apply, temps in HBM laid out over their domains.
+int compileMulti(hg_plan &p) {
+  const hg_program &g = p.prog;
+  const int es = g.dtype == HG_F32 ? 4 : 8;
+  p.tmpLay.assign(static_cast<size_t>(g.ntemps), Layout{});
+  p.tmpPtr.assign(static_cast<size_t>(g.ntemps), nullptr);
+  for (int a = 0; a < g.napplies; ++a) {
+    const hg_apply &A = p.applies[static_cast<size_t>(a)];
+    for (int k = 0; k < A.nresults; ++k) {
+      const int t = A.result_temp[k];
+      Layout L = makeLayout(A.domain, g.rank, es, A.domain.lb[g.rank - 1]);
+      p.tmpLay[static_cast<size_t>(t)] = L;
+      int st = cudaCheck(cudaMalloc(&p.tmpPtr[static_cast<size_t>(t)], L.bytes()),
+                         "cudaMalloc(temp)");
+      if (st)
+        return st;
+      cudaMemset(p.tmpPtr[static_cast<size_t>(t)], 0, L.bytes());
+    }
+  }
+  p.multi.clear();
+  for (int a = 0; a < g.napplies; ++a) {
+    const hg_apply &A = p.applies[static_cast<size_t>(a)];
+    std::vector<const Layout *> lay;
+    for (int o = 0; o < A.noperands; ++o)
+      lay.push_back(A.operand[o] >= 0 ? &p.lay[static_cast<size_t>(A.operand[o])]
+                                      : &p.tmpLay[static_cast<size_t>(-A.operand[o] - 1)]);
+    hg_plan::MultiApply M;
+    std::vector<GOp> out;
+    int st = compileSlice(g.rank, g.ops + A.op_begin, A.nops, A.result_op, A.nresults, lay, out,
+                          M.nslots, M.resSlot);
+    if (st)
+      return st;
+    st = uploadOps(out, &M.ops);
+    if (st)
+      return st;
+    p.multi.push_back(M);
+  }
+  return HG_OK;
+}
+
+int multiStep(hg_plan &p, cudaStream_t st) {
+  const hg_program &g = p.prog;
+  for (int a = 0; a < g.napplies; ++a) {
+    const hg_apply &A = p.applies[static_cast<size_t>(a)];
+    const hg_plan::MultiApply &M = p.multi[static_cast<size_t>(a)];
+    GenericLaunch L{};
+    L.dtype = g.dtype;
+    L.rank = g.rank;
+    for (int d = 0; d < g.rank; ++d) {
+      L.dom_lb[d] = A.domain.lb[d];
+      L.dom_ext[d] = A.domain.ub[d] - A.domain.lb[d];
+    }
+    L.nops = A.nops;
+    L.nslots = M.nslots;
+    L.noperands = A.noperands;
+    L.nresults = A.nresults;
+    L.ops_dev = M.ops;
+    for (int o = 0; o < A.noperands; ++o) {
+      if (A.operand[o] >= 0) {
+        const int b = p.bind[static_cast<size_t>(A.operand[o])];
+        L.op_base[o] = p.dptr[static_cast<size_t>(b)];
+        L.op_lay[o] = devLayout(p.lay[static_cast<size_t>(b)]);
+      } else {
+        const int t = -A.operand[o] - 1;
+        L.op_base[o] = p.tmpPtr[static_cast<size_t>(t)];
+        L.op_lay[o] = devLayout(p.tmpLay[static_cast<size_t>(t)]);
+      }
+    }
+    for (int k = 0; k < A.nresults; ++k) {
+      const int t = A.result_temp[k];
+      L.out_base[k] = p.tmpPtr[static_cast<size_t>(t)];
+      L.out_lay[k] = devLayout(p.tmpLay[static_cast<size_t>(t)]);
+      L.res_slot[k] = M.resSlot[static_cast<size_t>(k)];
+      for (int d = 0; d < 3; ++d) {
+        L.st_lb[k][d] = d < g.rank ? A.domain.lb[d] : 0;
+        L.st_ub[k][d] = d < g.rank ? A.domain.ub[d] : 1;
+      }
+    }
+    int rc = launchGeneric(L, st);
+    if (rc)
+      return rc;
+    ++p.launches;
+  }
+  for (int k = 0; k < g.nstores; ++k) { // stencil.store: temp region -> field
+    const int t = g.mstore_temp[k];
+    const int b = p.bind[static_cast<size_t>(g.mstore_field[k])];
+    int rc = launchCopyBox(p.tmpPtr[static_cast<size_t>(t)], devLayout(p.tmpLay[static_cast<size_t>(t)]),
+                           p.dptr[static_cast<size_t>(b)], devLayout(p.lay[static_cast<size_t>(b)]),
+                           g.mstore[k].lb, g.mstore[k].ub, st);
+    if (rc)
+      return rc;
+    ++p.launches;
+  }
+  return HG_OK;
 }
 
 } // namespace
@@ -111,7 +228,11 @@ int compileGeneric(hg_plan &p) {
 int planStep(hg_plan &p, cudaStream_t st) {
   const hg_program &g = p.prog;
   const Analysis &a = p.an;
-  if (a.family == Family::Star) {
+  if (a.family == Family::Multi) {
+    int rc = multiStep(p, st);
+    if (rc)
+      return rc;
+  } else if (a.family == Family::Star) {
     const StarSpec &s = a.star;
     const int bCur = p.bind[static_cast<size_t>(g.operand_field[s.cur_operand])];
     const int bPrev =
@@ -194,7 +315,8 @@ int planStep(hg_plan &p, cudaStream_t st) {
     if (st2)
       return st2;
   }
-  ++p.launches;
+  if (a.family != Family::Multi)
+    ++p.launches;
   // rotate (serial.cpp:83-85): next[i] = binding[src[i]]
   std::vector<int> nxt(p.bind.size());
   for (size_t i = 0; i < p.bind.size(); ++i)
@@ -234,6 +356,10 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
   p->prog = *prog;
   p->ops.assign(prog->ops, prog->ops + std::max(prog->nops, 0));
   p->prog.ops = p->ops.data();
+  if (prog->napplies > 0 && prog->applies) {
+    p->applies.assign(prog->applies, prog->applies + prog->napplies);
+    p->prog.applies = p->applies.data();
+  }
   int st = analyze(p->prog, p->an);
   if (st)
     return st;
@@ -257,7 +383,7 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
   if (st)
     return st;
   const int es = g.dtype == HG_F32 ? 4 : 8;
-  const int64_t coreLast = g.store[0].lb[g.rank - 1];
+  const int64_t coreLast = storedRegion(g, 0).lb[g.rank - 1];
   for (int f = 0; f < g.nfields; ++f) {
     Layout L = makeLayout(g.fields[f], g.rank, es, coreLast);
     void *ptr = nullptr;
@@ -269,6 +395,16 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
     st = cudaCheck(cudaMemset(ptr, 0, L.bytes()), "cudaMemset(field)");
     if (st)
       return st;
+  }
+  if (p->an.family == Family::Multi) {
+    st = compileMulti(*p);
+    if (st)
+      return st;
+    p->bind.resize(static_cast<size_t>(g.nfields));
+    for (int i = 0; i < g.nfields; ++i)
+      p->bind[static_cast<size_t>(i)] = i;
+    *out = p.release();
+    return HG_OK;
   }
   if (p->an.family == Family::Star && p->an.star.kind == kCopy)
     p->an.family = Family::Generic; // a plain copy needs no stencil machinery
@@ -325,6 +461,10 @@ int hg_plan_destroy(hg_plan *p) {
     cudaGraphExecDestroy(g.second);
   for (void *d : p->dptr)
     cudaFree(d);
+  for (void *d : p->tmpPtr)
+    cudaFree(d);
+  for (auto &m : p->multi)
+    cudaFree(m.ops);
   if (p->gopsDev)
     cudaFree(p->gopsDev);
   delete p;

@@ -33,6 +33,17 @@ struct hg_plan {
   std::shared_ptr<hg::JitKernel> jit;  // fused-apply family (generated, per program)
   std::vector<CUtensorMap> tmApply;   // per buffer, for the fused-apply boxes
   std::map<int, cudaGraphExec_t> graphs; // hg_plan_run: captured G-step graphs per phase
+  // multi-apply steps: the applies, their temps (HBM, laid out over their domains) and one
+  // compiled op slice per apply
+  std::vector<hg_apply> applies;
+  std::vector<hg::Layout> tmpLay;
+  std::vector<void *> tmpPtr;
+  struct MultiApply {
+    hg::GOp *ops = nullptr;
+    int nslots = 0;
+    std::vector<int> resSlot;
+  };
+  std::vector<MultiApply> multi;
 };
 
 namespace hg {

@@ -256,6 +256,84 @@ struct Matcher {
 
 } // namespace
 
+namespace {
+
+// Multi-apply steps (hg_apply list): operands are fields or earlier temps, regions are op
+// slices, every access stays inside its operand over the apply's domain, stores copy temps.
+int validateMulti(const hg_program &p) {
+  if (p.napplies > HG_MAX_APPLIES || !p.applies)
+    return setError(HG_EINVAL, "apply count out of range");
+  if (p.ntemps < 1 || p.ntemps > HG_MAX_TEMPS)
+    return setError(HG_EINVAL, "temp count out of range");
+  if (p.nstores < 1 || p.nstores > HG_MAX_STORES)
+    return setError(HG_EINVAL, "store count out of range");
+  if (p.noperands < 0 || p.noperands > HG_MAX_FIELDS)
+    return setError(HG_EINVAL, "load count out of range");
+  for (int o = 0; o < p.noperands; ++o)
+    if (p.operand_field[o] < 0 || p.operand_field[o] >= p.nfields)
+      return setError(HG_EINVAL, "stencil.load of a missing field");
+  std::vector<int> defined(static_cast<size_t>(p.ntemps), -1); // temp -> defining apply
+  for (int a = 0; a < p.napplies; ++a) {
+    const hg_apply &A = p.applies[a];
+    const std::string where = " (apply " + std::to_string(a) + ")";
+    if (A.noperands < 0 || A.noperands > HG_MAX_FIELDS || A.nresults < 1 ||
+        A.nresults > HG_MAX_RESULTS || A.nops < 1 || A.op_begin < 0 ||
+        A.op_begin + A.nops > p.nops)
+      return setError(HG_EINVAL, "malformed apply" + where);
+    for (int d = 0; d < p.rank; ++d)
+      if (A.domain.lb[d] >= A.domain.ub[d])
+        return setError(HG_EINVAL, "unresolved or empty stencil.apply bounds" + where);
+    for (int o = 0; o < A.noperands; ++o) {
+      const int x = A.operand[o];
+      if (x >= 0 ? x >= p.nfields : (-x - 1 >= p.ntemps || defined[static_cast<size_t>(-x - 1)] < 0))
+        return setError(HG_EINVAL, "apply operand is neither a loaded field nor an earlier "
+                                   "apply result" + where);
+    }
+    const hg_op *ops = p.ops + A.op_begin;
+    for (int i = 0; i < A.nops; ++i) {
+      const hg_op &o = ops[i];
+      if (o.code == HG_OP_ACCESS) {
+        if (o.operand < 0 || o.operand >= A.noperands)
+          return setError(HG_EINVAL, "stencil.access of a missing apply operand" + where);
+        const int x = A.operand[o.operand];
+        const hg_bounds &b = x >= 0 ? p.fields[x]
+                                    : p.applies[defined[static_cast<size_t>(-x - 1)]].domain;
+        for (int d = 0; d < p.rank; ++d)
+          if (A.domain.lb[d] + o.off[d] < b.lb[d] || A.domain.ub[d] + o.off[d] > b.ub[d])
+            return setError(HG_ETRAP, "stencil access escapes the value bounds" + where);
+      } else if (o.code >= HG_OP_ADD && o.code <= HG_OP_DIV) {
+        if (o.a < 0 || o.a >= i || o.b < 0 || o.b >= i)
+          return setError(HG_EINVAL, "use before def in the apply region" + where);
+      } else if (o.code != HG_OP_CONST) {
+        return setError(HG_EINVAL, "unknown op code" + where);
+      }
+    }
+    for (int k = 0; k < A.nresults; ++k) {
+      const int t = A.result_temp[k];
+      if (A.result_op[k] < 0 || A.result_op[k] >= A.nops || t < 0 || t >= p.ntemps ||
+          defined[static_cast<size_t>(t)] >= 0)
+        return setError(HG_EINVAL, "malformed apply results" + where);
+      defined[static_cast<size_t>(t)] = a;
+    }
+  }
+  for (int k = 0; k < p.nstores; ++k) {
+    const int t = p.mstore_temp[k], f = p.mstore_field[k];
+    if (t < 0 || t >= p.ntemps || defined[static_cast<size_t>(t)] < 0 || f < 0 || f >= p.nfields)
+      return setError(HG_EINVAL, "stencil.store of an undefined temp or into a missing field");
+    const hg_bounds &dom = p.applies[defined[static_cast<size_t>(t)]].domain;
+    for (int d = 0; d < p.rank; ++d) {
+      if (p.mstore[k].lb[d] >= p.mstore[k].ub[d])
+        return setError(HG_EINVAL, "empty store region");
+      if (p.mstore[k].lb[d] < p.fields[f].lb[d] || p.mstore[k].ub[d] > p.fields[f].ub[d] ||
+          p.mstore[k].lb[d] < dom.lb[d] || p.mstore[k].ub[d] > dom.ub[d])
+        return setError(HG_ETRAP, "store region escapes the field bounds");
+    }
+  }
+  return HG_OK;
+}
+
+} // namespace
+
 int validateProgram(const hg_program &p) {
   if (p.rank < 1 || p.rank > HG_MAX_RANK)
     return setError(HG_EINVAL, "program rank must be 1, 2, or 3");
@@ -263,6 +341,18 @@ int validateProgram(const hg_program &p) {
     return setError(HG_EINVAL, "program dtype must be f32 or f64");
   if (p.nfields < 1 || p.nfields > HG_MAX_FIELDS)
     return setError(HG_EINVAL, "field count out of range");
+  if (p.napplies > 0) {
+    if (p.nops < 1 || p.nops > HG_MAX_OPS || !p.ops)
+      return setError(HG_EINVAL, "apply region op count out of range");
+    for (int f = 0; f < p.nfields; ++f)
+      for (int d = 0; d < p.rank; ++d)
+        if (p.fields[f].lb[d] >= p.fields[f].ub[d])
+          return setError(HG_EINVAL, "field " + std::to_string(f) + " has empty bounds");
+    int st = validateMulti(p);
+    if (st)
+      return st;
+    goto time_slots;
+  }
   if (p.noperands < 0 || p.noperands > HG_MAX_FIELDS)
     return setError(HG_EINVAL, "apply operand count out of range");
   if (p.nops < 1 || p.nops > HG_MAX_OPS || !p.ops)
@@ -311,7 +401,7 @@ int validateProgram(const hg_program &p) {
     }
   }
   // time slots: stencil_transforms.cpp:196-230
-  {
+time_slots : {
     bool seen[HG_MAX_FIELDS] = {};
     int at = 0;
     if (p.ngroups < 0 || p.ngroups > HG_MAX_FIELDS)
@@ -336,6 +426,35 @@ int analyze(const hg_program &p, Analysis &a) {
   int st = validateProgram(p);
   if (st)
     return st;
+  if (p.napplies > 0) {
+    // rotation + a generic launch per apply (temps materialised over their domains)
+    for (int k = 0; k < p.nstores; ++k)
+      for (int a2 = 0; a2 < p.napplies; ++a2)
+        for (int o = 0; o < p.applies[a2].noperands; ++o)
+          if (p.applies[a2].operand[o] == p.mstore_field[k])
+            return setError(HG_EUNSUPPORTED,
+                            "stencil.store into a field the step loads (in-place update) is not "
+                            "supported by the device path");
+    a.src.assign(static_cast<size_t>(p.nfields), 0);
+    for (int i = 0; i < p.nfields; ++i)
+      a.src[static_cast<size_t>(i)] = i;
+    int at = 0;
+    a.period = 1;
+    for (int g = 0; g < p.ngroups; ++g) {
+      for (int j = 0; j < p.group_len[g]; ++j)
+        a.src[static_cast<size_t>(p.groups[at + j])] = p.groups[at + (j + 1) % p.group_len[g]];
+      a.period = a.period / gcdInt(a.period, p.group_len[g]) * p.group_len[g];
+      at += p.group_len[g];
+    }
+    for (int d = 0; d < p.rank; ++d) {
+      a.dom_lb[d] = p.applies[0].domain.lb[d];
+      a.dom_ub[d] = p.applies[0].domain.ub[d];
+    }
+    a.family = Family::Multi;
+    a.name = "multi" + std::to_string(p.napplies) + "x_generic" + std::to_string(p.rank) + "d_" +
+             (p.dtype == HG_F32 ? "f32" : "f64");
+    return HG_OK;
+  }
   // apply domain = hull of the store regions
   for (int d = 0; d < p.rank; ++d) {
     a.dom_lb[d] = p.store[0].lb[d];
@@ -709,10 +828,13 @@ int hg_decompose_program(const hg_program *global, int ndim, const int64_t *grid
     return st;
   const hg_program &g = *global;
   int r = g.rank;
+  const bool multi = g.napplies > 0;
+  const int nst = multi ? g.nstores : g.nresults;
+  const hg_bounds *stores = multi ? g.mstore : g.store;
   // the domain: every store covers the same region (:121-140)
-  for (int k = 1; k < g.nresults; ++k)
+  for (int k = 1; k < nst; ++k)
     for (int d = 0; d < r; ++d)
-      if (g.store[k].lb[d] != g.store[0].lb[d] || g.store[k].ub[d] != g.store[0].ub[d])
+      if (stores[k].lb[d] != stores[0].lb[d] || stores[k].ub[d] != stores[0].ub[d])
         return setError(HG_EINVAL, "decompose requires every store to cover the same domain");
   if (ndim != r)
     return setError(HG_EINVAL, "grid rank " + std::to_string(ndim) +
@@ -721,30 +843,40 @@ int hg_decompose_program(const hg_program *global, int ndim, const int64_t *grid
   for (int d = 0; d < r; ++d) {
     if (grid[d] < 1)
       return setError(HG_EINVAL, "grid dimensions must be at least 1");
-    int64_t ext = g.store[0].ub[d] - g.store[0].lb[d];
+    int64_t ext = stores[0].ub[d] - stores[0].lb[d];
     if (ext % grid[d] != 0)
       return setError(HG_EINVAL, "domain extent " + std::to_string(ext) + " in dimension " +
                                      std::to_string(d) + " is not divisible by grid extent " +
                                      std::to_string(grid[d]));
     core[d] = ext / grid[d];
-    clb[d] = g.store[0].lb[d];
+    clb[d] = stores[0].lb[d];
   }
-  // face footprints only (:167-200)
-  for (int i = 0; i < g.nops; ++i)
-    if (g.ops[i].code == HG_OP_ACCESS) {
-      int nz = 0;
-      for (int d = 0; d < r; ++d)
-        nz += g.ops[i].off[d] != 0;
-      if (nz > 1)
-        return setError(HG_EINVAL, "decompose supports face footprints only; a diagonal "
-                                   "access offset requires corner exchanges");
-    }
+  // per apply: no apply-result operand, face footprints only (:164-200)
+  const int napp = multi ? g.napplies : 1;
+  for (int a = 0; a < napp; ++a) {
+    const int b = multi ? g.applies[a].op_begin : 0;
+    const int n = multi ? g.applies[a].nops : g.nops;
+    if (multi)
+      for (int o = 0; o < g.applies[a].noperands; ++o)
+        if (g.applies[a].operand[o] < 0)
+          return setError(HG_EINVAL,
+                          "decompose does not support an apply consuming another apply");
+    for (int i = b; i < b + n; ++i)
+      if (g.ops[i].code == HG_OP_ACCESS) {
+        int nz = 0;
+        for (int d = 0; d < r; ++d)
+          nz += g.ops[i].off[d] != 0;
+        if (nz > 1)
+          return setError(HG_EINVAL, "decompose supports face footprints only; a diagonal "
+                                     "access offset requires corner exchanges");
+      }
+  }
   // per-field symmetric halos, <= core (:200-243)
   int64_t below[HG_MAX_FIELDS][3] = {}, above[HG_MAX_FIELDS][3] = {};
   for (int f = 0; f < g.nfields; ++f)
     for (int d = 0; d < r; ++d) {
-      below[f][d] = g.store[0].lb[d] - g.fields[f].lb[d];
-      above[f][d] = g.fields[f].ub[d] - g.store[0].ub[d];
+      below[f][d] = stores[0].lb[d] - g.fields[f].lb[d];
+      above[f][d] = g.fields[f].ub[d] - stores[0].ub[d];
       if (below[f][d] < 0 || above[f][d] < 0)
         return setError(HG_EINVAL, "field bounds do not cover the stored domain");
       if (below[f][d] != above[f][d])
@@ -758,18 +890,37 @@ int hg_decompose_program(const hg_program *global, int ndim, const int64_t *grid
       out.fields[f].lb[d] = clb[d] - below[f][d];
       out.fields[f].ub[d] = clb[d] + core[d] + above[f][d];
     }
-  for (int k = 0; k < g.nresults; ++k)
+  for (int k = 0; k < nst; ++k)
     for (int d = 0; d < r; ++d) {
-      out.store[k].lb[d] = clb[d];
-      out.store[k].ub[d] = clb[d] + core[d];
+      hg_bounds &sb = multi ? out.mstore[k] : out.store[k];
+      sb.lb[d] = clb[d];
+      sb.ub[d] = clb[d] + core[d];
     }
+  if (multi) {
+    // propagate-bounds on the local shapes (:309-311): an apply no other apply reads is
+    // evaluated exactly over what is stored of it, i.e. the local core; the rewritten
+    // apply list lives in the caller's local->applies buffer (napplies entries)
+    hg_apply *la = const_cast<hg_apply *>(local->applies);
+    if (!la || la == g.applies)
+      return setError(HG_EINVAL, "decompose of a multi-apply step needs local->applies set "
+                                 "to a caller buffer of napplies entries");
+    for (int a = 0; a < g.napplies; ++a) {
+      la[a] = g.applies[a];
+      for (int d = 0; d < r; ++d) {
+        la[a].domain.lb[d] = clb[d];
+        la[a].domain.ub[d] = clb[d] + core[d];
+      }
+    }
+    out.applies = la;
+  }
   std::memset(dc, 0, sizeof *dc);
   dc->ndim = ndim;
   for (int d = 0; d < r; ++d) {
     dc->grid[d] = grid[d];
     dc->core[d] = core[d];
   }
-  // a swap before every load (:276-300), template exchanges (no coord)
+  // a swap before every load (:276-300), template exchanges (no coord); the single-apply
+  // form's operands are its loads, the multi-apply form lists them in operand_field
   for (int o = 0; o < g.noperands; ++o) {
     hg_swap &s = dc->swaps[dc->nswaps++];
     int f = g.operand_field[o];

@@ -295,9 +295,28 @@ void skipAttr(Reader &R) {
     parseType(R);
 }
 
+struct PApply {
+  std::vector<int> operands;  // >= 0 field, < 0 temp (-t-1)
+  int op_begin = 0, nops = 0;
+  std::vector<int> result_op; // slice-relative
+  std::vector<int> result_temp;
+  bool domainKnown = false;
+  hg_bounds domain{};
+};
+
+struct PStore {
+  int temp, field;
+  hg_bounds region;
+};
+
 struct Parsed {
   hg_program prog{};
   std::vector<hg_op> ops;
+  std::vector<hg_apply> applies;
+  std::vector<PApply> papplies;
+  std::vector<PStore> pstores;
+  std::vector<int> loads; // stencil.load fields in step order
+  int ntemps = 0;
   hg_decomp dc{};
   bool decomposed = false;
   std::string reference; // dmp.reference text, if any
@@ -385,8 +404,10 @@ void parseModule(const std::string &text, Parsed &P) {
       }
       argIdx[argNames[static_cast<size_t>(f)]] = f;
     }
-    std::map<std::string, int> applyResult; // result value -> result index
-    int napply = 0;
+    std::map<std::string, int> tempOf; // apply result value -> temp id
+    int &ntemps = P.ntemps;
+    std::vector<PApply> &applies = P.papplies;
+    std::vector<PStore> &stores = P.pstores;
     R.expect("{");
     while (!R.accept("}")) {
       if (R.peek("func.return")) {
@@ -443,19 +464,15 @@ void parseModule(const std::string &text, Parsed &P) {
         R.expect("to");
         std::string dst = R.value();
         std::string b = R.balanced('(', ')');
-        auto rit = applyResult.find(src);
+        auto rit = tempOf.find(src);
         auto fit = argIdx.find(dst);
-        if (rit == applyResult.end() || fit == argIdx.end())
+        if (rit == tempOf.end() || fit == argIdx.end())
           R.fail("stencil.store of a non-apply value or into a non-argument");
-        int64_t lb[3], ub[3];
-        int r = parseBoundsText(R, b.substr(1, b.size() - 2), lb, ub);
+        PStore st{rit->second, fit->second, {}};
+        int r = parseBoundsText(R, b.substr(1, b.size() - 2), st.region.lb, st.region.ub);
         if (r != p.rank)
           R.fail("store bounds rank mismatch");
-        p.store_field[rit->second] = fit->second;
-        for (int d = 0; d < r; ++d) {
-          p.store[rit->second].lb[d] = lb[d];
-          p.store[rit->second].ub[d] = ub[d];
-        }
+        stores.push_back(st);
         R.expect(":");
         parseType(R);
         R.expect("to");
@@ -475,6 +492,7 @@ void parseModule(const std::string &text, Parsed &P) {
         if (it == argIdx.end())
           R.fail("stencil.load of a non-argument");
         loadOf[defs[0]] = it->second;
+        P.loads.push_back(it->second);
         R.expect(":");
         parseType(R);
         R.expect("->");
@@ -483,8 +501,11 @@ void parseModule(const std::string &text, Parsed &P) {
       }
       if (opn != "stencil.apply")
         R.fail("unsupported op in the step function: " + opn);
-      if (++napply > 1)
-        R.fail("more than one stencil.apply per step");
+      if (applies.size() >= HG_MAX_APPLIES)
+        R.fail("too many stencil.apply ops");
+      applies.emplace_back();
+      PApply &A = applies.back();
+      A.op_begin = static_cast<int>(P.ops.size());
       R.expect("(");
       std::map<std::string, int> regionArg;
       if (!R.accept(")")) {
@@ -495,36 +516,62 @@ void parseModule(const std::string &text, Parsed &P) {
           R.expect(":");
           parseType(R);
           auto it = loadOf.find(t);
-          if (it == loadOf.end())
-            R.fail("apply operand is not a stencil.load result");
-          regionArg[a] = p.noperands;
-          p.operand_field[p.noperands++] = it->second;
+          auto tt = tempOf.find(t);
+          if (it != loadOf.end())
+            A.operands.push_back(it->second);
+          else if (tt != tempOf.end())
+            A.operands.push_back(-tt->second - 1);
+          else
+            R.fail("apply operand is neither a stencil.load nor an apply result");
+          regionArg[a] = static_cast<int>(A.operands.size()) - 1;
         } while (R.accept(","));
         R.expect(")");
+        if (A.operands.size() > HG_MAX_FIELDS)
+          R.fail("too many apply operands");
       }
       R.expect("->");
-      parseType(R);
-      for (size_t k = 0; k < defs.size(); ++k)
-        applyResult[defs[k]] = static_cast<int>(k);
-      p.nresults = static_cast<int>(defs.size());
-      if (p.nresults > HG_MAX_RESULTS)
+      {
+        // result type(s): a single !temp or a (tuple); bounds give the evaluation domain
+        R.ws();
+        std::string rt;
+        if (R.peek("(")) {
+          rt = R.balanced('(', ')');
+          Reader R2(rt);
+          R2.expect("(");
+          TypeInfo t0 = parseType(R2);
+          A.domainKnown = t0.known;
+          for (int d = 0; d < t0.rank; ++d) {
+            A.domain.lb[d] = t0.lb[d];
+            A.domain.ub[d] = t0.ub[d];
+          }
+        } else {
+          TypeInfo t0 = parseType(R);
+          A.domainKnown = t0.known;
+          for (int d = 0; d < t0.rank; ++d) {
+            A.domain.lb[d] = t0.lb[d];
+            A.domain.ub[d] = t0.ub[d];
+          }
+        }
+      }
+      if (defs.size() > HG_MAX_RESULTS)
         R.fail("too many apply results");
+      for (size_t k = 0; k < defs.size(); ++k) {
+        A.result_temp.push_back(ntemps);
+        tempOf[defs[k]] = ntemps++;
+      }
       std::map<std::string, int> vid;
       R.expect("{");
       while (!R.accept("}")) {
         if (R.peek("stencil.return")) {
           R.expect("stencil.return");
-          int k = 0;
           do {
             std::string v = R.value();
             auto it = vid.find(v);
             if (it == vid.end())
               R.fail("stencil.return of an undefined value %" + v);
-            if (k >= p.nresults)
-              R.fail("stencil.return arity mismatch");
-            p.result_op[k++] = it->second;
+            A.result_op.push_back(it->second - A.op_begin);
           } while (R.accept(","));
-          if (k != p.nresults)
+          if (A.result_op.size() != A.result_temp.size())
             R.fail("stencil.return arity mismatch");
           R.expect(":");
           do
@@ -585,8 +632,8 @@ void parseModule(const std::string &text, Parsed &P) {
           auto ia = vid.find(a), ib = vid.find(b);
           if (ia == vid.end() || ib == vid.end())
             R.fail("use before def in the apply region");
-          h.a = ia->second;
-          h.b = ib->second;
+          h.a = ia->second - A.op_begin;
+          h.b = ib->second - A.op_begin;
           R.expect(":");
           parseType(R);
         } else {
@@ -597,12 +644,74 @@ void parseModule(const std::string &text, Parsed &P) {
         vid[d] = static_cast<int>(P.ops.size());
         P.ops.push_back(h);
       }
+      A.nops = static_cast<int>(P.ops.size()) - A.op_begin;
     }
   }
   if (!haveEntry)
     R.fail("module has no single all-field step function");
   hg_program &p = P.prog;
   p.nops = static_cast<int>(P.ops.size());
+  if (P.papplies.empty())
+    R.fail("step function has no stencil.apply");
+  bool chained = false;
+  for (auto &A : P.papplies)
+    for (int x : A.operands)
+      chained = chained || x < 0;
+  if (P.papplies.size() == 1 && !chained) {
+    // the single-apply form: operands are loads, results are stored directly
+    const PApply &A = P.papplies[0];
+    p.noperands = static_cast<int>(A.operands.size());
+    for (int o = 0; o < p.noperands; ++o)
+      p.operand_field[o] = A.operands[static_cast<size_t>(o)];
+    p.nresults = static_cast<int>(A.result_op.size());
+    for (int k = 0; k < p.nresults; ++k)
+      p.result_op[k] = A.result_op[static_cast<size_t>(k)];
+    std::vector<char> stored(static_cast<size_t>(p.nresults), 0);
+    for (const PStore &st : P.pstores) {
+      if (st.temp >= p.nresults || stored[static_cast<size_t>(st.temp)])
+        R.fail("each apply result must be stored exactly once");
+      stored[static_cast<size_t>(st.temp)] = 1;
+      p.store_field[st.temp] = st.field;
+      p.store[st.temp] = st.region;
+    }
+    for (char c : stored)
+      if (!c)
+        R.fail("an apply result is never stored");
+  } else {
+    for (const PApply &A : P.papplies) {
+      if (!A.domainKnown)
+        R.fail("unresolved stencil.apply bounds (run propagate-bounds)");
+      hg_apply h;
+      std::memset(&h, 0, sizeof h);
+      h.noperands = static_cast<int>(A.operands.size());
+      for (int o = 0; o < h.noperands; ++o)
+        h.operand[o] = A.operands[static_cast<size_t>(o)];
+      h.op_begin = A.op_begin;
+      h.nops = A.nops;
+      h.nresults = static_cast<int>(A.result_op.size());
+      for (int k = 0; k < h.nresults; ++k) {
+        h.result_op[k] = A.result_op[static_cast<size_t>(k)];
+        h.result_temp[k] = A.result_temp[static_cast<size_t>(k)];
+      }
+      h.domain = A.domain;
+      P.applies.push_back(h);
+    }
+    p.napplies = static_cast<int>(P.applies.size());
+    p.ntemps = P.ntemps;
+    if (P.loads.size() > HG_MAX_FIELDS)
+      R.fail("too many loads");
+    p.noperands = static_cast<int>(P.loads.size());
+    for (int o = 0; o < p.noperands; ++o)
+      p.operand_field[o] = P.loads[static_cast<size_t>(o)];
+    if (P.pstores.size() > HG_MAX_STORES)
+      R.fail("too many stores");
+    p.nstores = static_cast<int>(P.pstores.size());
+    for (int k = 0; k < p.nstores; ++k) {
+      p.mstore_temp[k] = P.pstores[static_cast<size_t>(k)].temp;
+      p.mstore_field[k] = P.pstores[static_cast<size_t>(k)].field;
+      p.mstore[k] = P.pstores[static_cast<size_t>(k)].region;
+    }
+  }
   int at = 0;
   for (auto &g : P.groups) {
     if (p.ngroups >= HG_MAX_FIELDS || at + static_cast<int>(g.size()) > HG_MAX_FIELDS)
@@ -618,7 +727,7 @@ void parseModule(const std::string &text, Parsed &P) {
         P.dc.grid[d] = topology[d];
     }
     for (int d = 0; d < p.rank; ++d)
-      P.dc.core[d] = p.store[0].ub[d] - p.store[0].lb[d];
+      P.dc.core[d] = storedRegion(p, 0).ub[d] - storedRegion(p, 0).lb[d];
   }
 }
 
@@ -628,8 +737,8 @@ void parseModule(const std::string &text, Parsed &P) {
 using namespace hg;
 
 extern "C" int hg_parse_program(const char *text, hg_program *prog, hg_op *ops, int cap_ops,
-                                hg_decomp *decomp, int *decomposed, char *reference,
-                                size_t ref_cap) {
+                                hg_apply *applies, int cap_applies, hg_decomp *decomp,
+                                int *decomposed, char *reference, size_t ref_cap) {
   if (!text || !prog || !ops)
     return setError(HG_EINVAL, "null argument");
   Parsed P;
@@ -643,8 +752,14 @@ extern "C" int hg_parse_program(const char *text, hg_program *prog, hg_op *ops, 
   if (static_cast<int>(P.ops.size()) > cap_ops)
     return setError(HG_EINVAL, "op buffer too small");
   std::memcpy(ops, P.ops.data(), P.ops.size() * sizeof(hg_op));
+  if (!P.applies.empty()) {
+    if (!applies || static_cast<int>(P.applies.size()) > cap_applies)
+      return setError(HG_EINVAL, "apply buffer too small");
+    std::memcpy(applies, P.applies.data(), P.applies.size() * sizeof(hg_apply));
+  }
   *prog = P.prog;
   prog->ops = ops;
+  prog->applies = P.applies.empty() ? nullptr : applies;
   if (decomp)
     *decomp = P.dc;
   if (decomposed)

@@ -113,6 +113,155 @@ AUTHORED = {
 """,
 }
 
+# Multi-apply modules (one apply consuming another's result temp, several results, and
+# independent applies in one step) -- the stencil-level form the reference interprets
+# apply by apply (interpreter.cpp stencil.apply / stencil.store handlers).
+AUTHORED["flux2_2d"] = """builtin.module attributes {stencil.time_slots = [[0, 1]]} {
+  func.func @flux(%u : !field<[-2,34]x[-2,26]xf32>, %v : !field<[-2,34]x[-2,26]xf32>) {
+    %t = stencil.load %u : !field<[-2,34]x[-2,26]xf32> -> !temp<?xf32>
+    %f = stencil.apply(%a = %t : !temp<?xf32>) -> !temp<?xf32> {
+      %c = stencil.access %a[0,0] : f32
+      %e = stencil.access %a[1,0] : f32
+      %d = arith.subf %e, %c : f32
+      %k = arith.constant 0.3 : f32
+      %r = arith.mulf %d, %k : f32
+      stencil.return %r : f32
+    }
+    %o = stencil.apply(%b = %f : !temp<?xf32>, %x = %t : !temp<?xf32>) -> !temp<?xf32> {
+      %fp = stencil.access %b[0,0] : f32
+      %fm = stencil.access %b[-1,0] : f32
+      %df = arith.subf %fp, %fm : f32
+      %xc = stencil.access %x[0,1] : f32
+      %xs = arith.addf %xc, %df : f32
+      stencil.return %xs : f32
+    }
+    stencil.store %o to %v ([0,32]x[0,24]) : !temp<?xf32> to !field<[-2,34]x[-2,26]xf32>
+    func.return
+  }
+}
+"""
+AUTHORED["chain3_3d_f64"] = """builtin.module attributes {stencil.time_slots = [[0, 2]]} {
+  func.func @chain(%u : !field<[-1,13]x[-2,12]x[-1,17]xf64>, %w : !field<[-1,13]x[-2,12]x[-1,17]xf64>, %un : !field<[-1,13]x[-2,12]x[-1,17]xf64>, %s : !field<[-1,13]x[-2,12]x[-1,17]xf64>) {
+    %tu = stencil.load %u : !field<[-1,13]x[-2,12]x[-1,17]xf64> -> !temp<?xf64>
+    %tw = stencil.load %w : !field<[-1,13]x[-2,12]x[-1,17]xf64> -> !temp<?xf64>
+    %gx, %gy = stencil.apply(%a = %tu : !temp<?xf64>) -> (!temp<?xf64>, !temp<?xf64>) {
+      %c = stencil.access %a[0,0,0] : f64
+      %xp = stencil.access %a[1,0,0] : f64
+      %yp = stencil.access %a[0,1,0] : f64
+      %dx = arith.subf %xp, %c : f64
+      %dy = arith.subf %yp, %c : f64
+      stencil.return %dx, %dy : f64, f64
+    }
+    %m = stencil.apply(%p = %gx : !temp<?xf64>, %q = %gy : !temp<?xf64>, %r = %tw : !temp<?xf64>) -> !temp<?xf64> {
+      %px = stencil.access %p[0,0,0] : f64
+      %pm = stencil.access %p[-1,0,0] : f64
+      %qy = stencil.access %q[0,0,0] : f64
+      %qm = stencil.access %q[0,-1,0] : f64
+      %rz = stencil.access %r[0,0,1] : f64
+      %lx = arith.subf %px, %pm : f64
+      %ly = arith.subf %qy, %qm : f64
+      %l = arith.addf %lx, %ly : f64
+      %h = arith.constant 0.125 : f64
+      %hl = arith.mulf %h, %l : f64
+      %o1 = arith.addf %rz, %hl : f64
+      stencil.return %o1 : f64
+    }
+    %k = stencil.apply(%z = %tw : !temp<?xf64>) -> !temp<?xf64> {
+      %zc = stencil.access %z[0,0,0] : f64
+      %zm = stencil.access %z[0,-2,-1] : f64
+      %zd = arith.divf %zm, %zc : f64
+      stencil.return %zd : f64
+    }
+    stencil.store %m to %un ([0,12]x[0,10]x[0,16]) : !temp<?xf64> to !field<[-1,13]x[-2,12]x[-1,17]xf64>
+    stencil.store %k to %s ([0,12]x[0,10]x[0,16]) : !temp<?xf64> to !field<[-1,13]x[-2,12]x[-1,17]xf64>
+    func.return
+  }
+}
+"""
+AUTHORED["indep2_2d"] = """builtin.module {
+  func.func @two(%a : !field<[-1,41]x[-1,9]xf32>, %b : !field<[-1,41]x[-1,9]xf32>, %c : !field<[-1,41]x[-1,9]xf32>, %d : !field<[-1,41]x[-1,9]xf32>) {
+    %ta = stencil.load %a : !field<[-1,41]x[-1,9]xf32> -> !temp<?xf32>
+    %tb = stencil.load %b : !field<[-1,41]x[-1,9]xf32> -> !temp<?xf32>
+    %o1 = stencil.apply(%x = %ta : !temp<?xf32>) -> !temp<?xf32> {
+      %x0 = stencil.access %x[-1,1] : f32
+      %x1 = stencil.access %x[1,-1] : f32
+      %x2 = arith.addf %x0, %x1 : f32
+      stencil.return %x2 : f32
+    }
+    %o2 = stencil.apply(%y = %tb : !temp<?xf32>, %yy = %ta : !temp<?xf32>) -> !temp<?xf32> {
+      %y0 = stencil.access %y[0,0] : f32
+      %y1 = stencil.access %yy[0,1] : f32
+      %y2 = arith.mulf %y0, %y1 : f32
+      stencil.return %y2 : f32
+    }
+    stencil.store %o1 to %c ([0,40]x[0,8]) : !temp<?xf32> to !field<[-1,41]x[-1,9]xf32>
+    stencil.store %o2 to %d ([0,40]x[0,8]) : !temp<?xf32> to !field<[-1,41]x[-1,9]xf32>
+    func.return
+  }
+}
+"""
+
+# Decomposable multi-apply modules (independent applies, face footprints, symmetric halos):
+# decompose inserts a swap before every load (dmp_transforms.cpp:276-300).
+DECOMP_AUTHORED = {
+    "indep2f_2d": ("""builtin.module attributes {stencil.time_slots = [[0, 2], [1, 3]]} {
+  func.func @two(%a : !field<[-1,41]x[-1,9]xf32>, %b : !field<[-1,41]x[-1,9]xf32>, %c : !field<[-1,41]x[-1,9]xf32>, %d : !field<[-1,41]x[-1,9]xf32>) {
+    %ta = stencil.load %a : !field<[-1,41]x[-1,9]xf32> -> !temp<?xf32>
+    %tb = stencil.load %b : !field<[-1,41]x[-1,9]xf32> -> !temp<?xf32>
+    %o1 = stencil.apply(%x = %ta : !temp<?xf32>) -> !temp<?xf32> {
+      %x0 = stencil.access %x[-1,0] : f32
+      %x1 = stencil.access %x[0,-1] : f32
+      %x2 = arith.addf %x0, %x1 : f32
+      %x3 = arith.constant 0.5 : f32
+      %x4 = arith.mulf %x2, %x3 : f32
+      stencil.return %x4 : f32
+    }
+    %o2 = stencil.apply(%y = %tb : !temp<?xf32>, %yy = %ta : !temp<?xf32>) -> !temp<?xf32> {
+      %y0 = stencil.access %y[1,0] : f32
+      %y1 = stencil.access %yy[0,1] : f32
+      %y2 = arith.subf %y0, %y1 : f32
+      stencil.return %y2 : f32
+    }
+    stencil.store %o1 to %c ([0,40]x[0,8]) : !temp<?xf32> to !field<[-1,41]x[-1,9]xf32>
+    stencil.store %o2 to %d ([0,40]x[0,8]) : !temp<?xf32> to !field<[-1,41]x[-1,9]xf32>
+    func.return
+  }
+}
+""", [2, 2], 3),
+    "twin3_3d_f64": ("""builtin.module attributes {stencil.time_slots = [[0, 2], [1, 3]]} {
+  func.func @twin(%u : !field<[-2,18]x[-1,13]x[-1,17]xf64>, %v : !field<[-2,18]x[-1,13]x[-1,17]xf64>, %un : !field<[-2,18]x[-1,13]x[-1,17]xf64>, %vn : !field<[-2,18]x[-1,13]x[-1,17]xf64>) {
+    %tv = stencil.load %v : !field<[-2,18]x[-1,13]x[-1,17]xf64> -> !temp<?xf64>
+    %tu = stencil.load %u : !field<[-2,18]x[-1,13]x[-1,17]xf64> -> !temp<?xf64>
+    %ou = stencil.apply(%a = %tu : !temp<?xf64>) -> !temp<?xf64> {
+      %c = stencil.access %a[0,0,0] : f64
+      %zp = stencil.access %a[2,0,0] : f64
+      %zm = stencil.access %a[-2,0,0] : f64
+      %yp = stencil.access %a[0,1,0] : f64
+      %xm = stencil.access %a[0,0,-1] : f64
+      %s1 = arith.addf %zp, %zm : f64
+      %s2 = arith.addf %yp, %xm : f64
+      %s3 = arith.addf %s1, %s2 : f64
+      %k = arith.constant 0.2 : f64
+      %s4 = arith.mulf %k, %s3 : f64
+      %s5 = arith.subf %s4, %c : f64
+      stencil.return %s5 : f64
+    }
+    %ov = stencil.apply(%p = %tv : !temp<?xf64>, %q = %tu : !temp<?xf64>) -> !temp<?xf64> {
+      %pc = stencil.access %p[0,0,1] : f64
+      %py = stencil.access %p[0,-1,0] : f64
+      %qz = stencil.access %q[1,0,0] : f64
+      %m = arith.mulf %pc, %qz : f64
+      %n = arith.divf %m, %py : f64
+      stencil.return %n : f64
+    }
+    stencil.store %ou to %un ([0,16]x[0,12]x[0,16]) : !temp<?xf64> to !field<[-2,18]x[-1,13]x[-1,17]xf64>
+    stencil.store %ov to %vn ([0,16]x[0,12]x[0,16]) : !temp<?xf64> to !field<[-2,18]x[-1,13]x[-1,17]xf64>
+    func.return
+  }
+}
+""", [2, 2, 2], 3),
+}
+
 sys.path.insert(0, REPO)
 from paper_2404_02218_b200.programs.pw_advection import xir as pw_xir  # noqa: E402
 
@@ -145,6 +294,27 @@ DECOMP = [  # (kind, rank, extent, order, f32, grid, T)
 
 def prog_json(prog, ops):
     r = prog.rank
+    if prog.napplies > 0:
+        aps = prog.applies
+        return {
+            "rank": r, "dtype": prog.dtype, "nfields": prog.nfields,
+            "fields": [[list(prog.fields[i].lb[:r]), list(prog.fields[i].ub[:r])]
+                       for i in range(prog.nfields)],
+            "ops": [[o.code, o.a, o.b, o.operand, list(o.off[:r]), "%016x" % o.bits]
+                    for o in ops[:prog.nops]],
+            "applies": [{"operands": list(aps[a].operand[:aps[a].noperands]),
+                         "op_begin": aps[a].op_begin, "nops": aps[a].nops,
+                         "result_op": list(aps[a].result_op[:aps[a].nresults]),
+                         "result_temp": list(aps[a].result_temp[:aps[a].nresults]),
+                         "domain": [list(aps[a].domain.lb[:r]), list(aps[a].domain.ub[:r])]}
+                        for a in range(prog.napplies)],
+            "loads": list(prog.operand_field[:prog.noperands]),
+            "ntemps": prog.ntemps,
+            "mstores": [[prog.mstore_temp[k], prog.mstore_field[k],
+                         list(prog.mstore[k].lb[:r]), list(prog.mstore[k].ub[:r])]
+                        for k in range(prog.nstores)],
+            "groups": _groups(prog),
+        }
     return {
         "rank": r, "dtype": prog.dtype, "nfields": prog.nfields,
         "fields": [[list(prog.fields[i].lb[:r]), list(prog.fields[i].ub[:r])]
@@ -271,6 +441,31 @@ def main():
                     "serial_fp": fps(ref, ser)})
         print("decomp", kind, rank, ext, order, grid, T, flush=True)
     out["decomposed"] = dec
+
+    # decomposed multi-apply modules (authored), same record shape + the global program
+    dau = []
+    for name, (text, grid, T) in DECOMP_AUTHORED.items():
+        mod = ref.pipeline(ref.parse(text), "propagate-bounds")
+        gprog, gops, _ = ref.export_program(mod)
+        gs = "x".join(str(g) for g in grid)
+        dmod = ref.pipeline(mod, "propagate-bounds,decompose grid=" + gs)
+        lprog, lops, dc = ref.export_program(dmod)
+        init = L.hr_initial_fields(mod)
+        res = L.hr_simulate(dmod, init, T, 0)
+        if not res:
+            raise RuntimeError(ref.err())
+        ser = L.hr_run_serial(mod, L.hr_bufs_clone(init), T)
+        mmod = ref.pipeline(mod, "propagate-bounds,decompose grid=" + gs + ",lower-dmp-to-mpi")
+        mres = L.hr_simulate(mmod, init, T, 0)
+        if not mres:
+            raise RuntimeError(ref.err())
+        dau.append({"name": name, "grid": grid, "T": T, "program": prog_json(gprog, gops),
+                    "local_program": prog_json(lprog, lops), "decomp": decomp_json(dc),
+                    "text": ref.print(dmod), "global_text": ref.print(mod),
+                    "init_fp": fps(ref, init), "sim_fp": fps(ref, res),
+                    "mpi_sim_fp": fps(ref, mres), "serial_fp": fps(ref, ser)})
+        print("decomp authored", name, grid, T, flush=True)
+    out["decomposed_authored"] = dau
 
     # dmp arithmetic (dmp_ops.cpp:21-115)
     dmp = {"exchanges": [], "neighbors": [], "slicing": [], "coords": []}

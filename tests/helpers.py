@@ -32,6 +32,26 @@ def decomp_from_json(j) -> capi.HgDecomp:
 def prog_to_json(prog: "hg.Program"):
     p = prog.prog
     r = p.rank
+    if p.napplies > 0:
+        aps = p.applies
+        return {
+            "rank": r, "dtype": p.dtype, "nfields": p.nfields,
+            "fields": [[list(p.fields[i].lb[:r]), list(p.fields[i].ub[:r])]
+                       for i in range(p.nfields)],
+            "ops": [[o.code, o.a, o.b, o.operand, list(o.off[:r]), "%016x" % o.bits]
+                    for o in prog.op_list()],
+            "applies": [{"operands": list(aps[a].operand[:aps[a].noperands]),
+                         "op_begin": aps[a].op_begin, "nops": aps[a].nops,
+                         "result_op": list(aps[a].result_op[:aps[a].nresults]),
+                         "result_temp": list(aps[a].result_temp[:aps[a].nresults]),
+                         "domain": [list(aps[a].domain.lb[:r]), list(aps[a].domain.ub[:r])]}
+                        for a in range(p.napplies)],
+            "loads": list(p.operand_field[:p.noperands]),
+            "ntemps": p.ntemps,
+            "mstores": [[p.mstore_temp[k], p.mstore_field[k], list(p.mstore[k].lb[:r]),
+                         list(p.mstore[k].ub[:r])] for k in range(p.nstores)],
+            "groups": prog.groups(),
+        }
     return {
         "rank": r, "dtype": p.dtype, "nfields": p.nfields,
         "fields": [[list(p.fields[i].lb[:r]), list(p.fields[i].ub[:r])] for i in range(p.nfields)],

@@ -103,6 +103,35 @@ def test_simulate_lowered_mpi_module(ref, adapter, spec, grid, T):
     assert _fps(ref, gpu) == _fps(ref, cpu)
 
 
+@pytest.mark.gpu
+def test_multi_apply_dropin(ref, adapter, golden):
+    # multi-apply modules (chained and independent applies) through the drop-in: serial runs
+    # and decomposed simulate, bitwise against the reference's executors in-process
+    n = 0
+    for c in golden["authored"]:
+        if "applies" not in c["program"]:
+            continue
+        mod = ref.parse(c["text"])
+        init = ref.L.hr_initial_fields(mod)
+        cpu = ref.L.hr_run_serial(mod, ref.L.hr_bufs_clone(init), c["T"])
+        err = C.create_string_buffer(512)
+        gpu = adapter.hga_run_serial(mod, ref.L.hr_bufs_clone(init), c["T"], err, 512)
+        assert gpu, err.value.decode()
+        assert _fps(ref, gpu) == _fps(ref, cpu), c["name"]
+        n += 1
+    for c in golden["decomposed_authored"]:
+        mod = ref.parse(c["global_text"])
+        dmod = ref.parse(c["text"])
+        init = ref.L.hr_initial_fields(mod)
+        cpu = ref.L.hr_simulate(dmod, init, c["T"], 0)
+        err = C.create_string_buffer(512)
+        gpu = adapter.hga_simulate(dmod, init, c["T"], err, 512)
+        assert gpu, err.value.decode()
+        assert _fps(ref, gpu) == _fps(ref, cpu), c["name"]
+        n += 1
+    assert n >= 5
+
+
 def test_adapter_errors_like_the_reference(ref, adapter):
     # wrong field count -> TrapError text (serial.cpp:68-69 analogue), never a crash
     mod = ref.build("heat", 2, 8, 2, True)

@@ -29,7 +29,7 @@ def test_hgrun_parse_errors_are_reported():
 @pytest.mark.gpu
 def test_hgrun_run_serial_matches_reference(golden, tmp_path):
     done = 0
-    for c in golden["serial"]:
+    for c in golden["serial"] + golden["authored"]:
         if not c.get("text") or c["T"] > 20:
             continue
         f = tmp_path / "m.xir"
@@ -37,14 +37,14 @@ def test_hgrun_run_serial_matches_reference(golden, tmp_path):
         r = _run(["run-serial", str(f), "-t", str(c["T"])])
         assert r.returncode == 0, r.stderr
         fps = [ln.split()[2] for ln in r.stdout.splitlines() if ln.startswith("field ")]
-        assert fps == [h.lstrip("0") or "0" for h in c["final_fp"]], c["spec"]
+        assert fps == [h.lstrip("0") or "0" for h in c["final_fp"]], c.get("name", c.get("spec"))
         done += 1
-    assert done >= 15
+    assert done >= 23
 
 
 @pytest.mark.gpu
 def test_hgrun_simulate_check(golden, tmp_path):
-    for c in golden["decomposed"]:
+    for c in golden["decomposed"] + golden["decomposed_authored"]:
         f = tmp_path / "d.xir"
         f.write_text(c["text"])
         r = _run(["simulate", str(f), "-t", str(c["T"]), "--check"])

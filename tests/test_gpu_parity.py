@@ -61,7 +61,8 @@ def test_authored_programs_bitwise(golden, monkeypatch, family):
     for c in golden["authored"]:
         prog = program_from_json(c["program"])
         init, fin, _, name = _plan_run(prog, c["T"])
-        want = family if prog.rank >= 2 else "generic"
+        want = ("multi" if "applies" in c["program"] else
+                family if prog.rank >= 2 else "generic")
         assert name.startswith(want), (c["name"], name)
         assert [fp_hex(a) for a in init] == c["init_fp"], c["name"]
         assert [fp_hex(a) for a in fin] == c["final_fp"], c["name"]
@@ -180,6 +181,25 @@ def test_simulate_matches_reference(golden):
         init = hg.initial_fields(prog)
         out = hg.simulate(prog, c["grid"], init, c["T"], devices=[0] * int(np.prod(c["grid"])))
         assert [fp_hex(b.data) for b in out] == c["sim_fp"], case_id(c)
+
+
+def test_simulate_multi_apply_matches_reference(golden, port):
+    # decomposed multi-apply steps (independent applies, a swap before every load): gathered
+    # result == the reference's simulate, and every rank's halos == the oracle's
+    for c in golden["decomposed_authored"]:
+        glob = program_from_json(c["program"])
+        init = hg.initial_fields(glob)
+        n = int(np.prod(c["grid"]))
+        out = hg.simulate(glob, c["grid"], init, c["T"], devices=[0] * n)
+        assert [fp_hex(b.data) for b in out] == c["sim_fp"], c["name"]
+        states = _sim_rank_states(glob, c["grid"], c["T"])
+        local, dc = glob.decompose(c["grid"])
+        arrays = port.initial_fields(glob)
+        lbs = [glob.field_bounds(i)[0] for i in range(glob.nfields)]
+        for rk in range(n):
+            want = port.simulate_rank_state(local, dc, arrays, lbs, c["T"], rk)
+            for g, o in zip(states[rk], want):
+                assert np.array_equal(g.view(np.uint8), o.view(np.uint8)), (c["name"], rk)
 
 
 def _sim_rank_states(prog, grid, T):

@@ -95,7 +95,8 @@ def test_kernel_family_matching(golden):
     assert fam[("heat", 3, 8, 0)] == "star3d_r4_heat_f64"
     assert fam[("heat", 1, 2, 1)] == "generic1d_f32"
     for c in golden["authored"]:
-        assert program_from_json(c["program"]).kernel_family().startswith("generic")
+        fam = program_from_json(c["program"]).kernel_family()
+        assert fam.startswith("multi" if "applies" in c["program"] else "generic"), fam
 
 
 def test_validation_errors():
@@ -138,7 +139,7 @@ def test_fused_apply_family_generates_and_compiles(golden):
         buf = C.create_string_buffer(1 << 20)
         n = C.c_size_t()
         rc = capi.lib().hg_apply_compile(C.byref(p.prog), buf, 1 << 20, C.byref(n))
-        if p.rank == 1:
+        if p.rank == 1 or "applies" in c["program"]:
             assert rc == capi.HG_EUNSUPPORTED
             continue
         assert rc == 0, capi.lib().hg_last_error()
@@ -208,3 +209,29 @@ def test_native_xir_reader_errors():
            "      %v = arith.addf %x, %x : f32\n      stencil.return %v : f32\n    }\n")
     with pytest.raises(capi.HgError, match="use before def"):
         hg.Program.parse(bad)
+
+
+def test_decompose_multi_apply_matches_reference(golden):
+    # our decompose on the multi-apply descriptor == the reference's pass (local program with
+    # rewritten apply domains, one swap per load in load order)
+    for c in golden["decomposed_authored"]:
+        glob = program_from_json(c["program"])
+        local, dc = glob.decompose(c["grid"])
+        assert prog_to_json(local) == c["local_program"], c["name"]
+        assert decomp_to_json(dc) == c["decomp"], c["name"]
+        prog, pdc, ref = hg.Program.parse(c["text"])          # the printed dmp-level module
+        assert prog_to_json(prog) == c["local_program"]
+        assert decomp_to_json(pdc) == c["decomp"]
+        g2, _, _ = hg.Program.parse(ref)
+        assert prog_to_json(g2) == c["program"]
+
+
+def test_decompose_rejects_chained_applies(golden):
+    for c in golden["authored"]:
+        j = c["program"]
+        if "applies" not in j or not any(x < 0 for a in j["applies"] for x in a["operands"]):
+            continue
+        p = program_from_json(j)
+        grid = [1] * p.rank
+        with pytest.raises(capi.HgError, match="apply consuming another apply"):
+            p.decompose(grid)

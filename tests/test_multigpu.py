@@ -5,6 +5,7 @@ import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -41,6 +42,26 @@ def test_ipc_dmp_two_ranks(args):
                "--nproc-per-node", str(nproc), os.path.join(REPO, "tools", "dmp_check.py")] + args
         if grid:
             cmd += ["--grid", grid]
+        r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,grids", [("indep2f_2d", ["2x1", "1x2", "2x2"]),
+                                        ("twin3_3d_f64", ["2x1x1", "1x1x2", "2x2x1"])])
+def test_ipc_dmp_multi_apply(name, grids):
+    # a step of several applies: one swap per load, every swapped field over NVLink
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    for grid in grids:
+        nproc = int(np.prod([int(x) for x in grid.split("x")]))
+        if nproc > n:
+            continue
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone",
+               "--nproc-per-node", str(nproc), os.path.join(REPO, "tools", "dmp_check.py"),
+               "--golden", name, "--grid", grid, "--T", "5", "--calls", "2,3"]
         r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
         assert "OK" in r.stdout

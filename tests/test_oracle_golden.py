@@ -125,3 +125,21 @@ def test_pack_unpack_roundtrip(port):
     port.unpack(b, lb, at, size, packed)
     assert np.array_equal(b[1:5, 2:7, 3:9], a[1:5, 2:7, 3:9])
     assert np.count_nonzero(b) == np.count_nonzero(a[1:5, 2:7, 3:9])
+
+
+def test_decomposed_multi_apply(golden, port):
+    # independent applies in one step, decomposed: a swap before every load (the reference's
+    # decompose, dmp_transforms.cpp:276-300), simulate == serial == lowered-mpi simulate
+    import paper_2404_02218_b200 as hg
+    assert len(golden["decomposed_authored"]) >= 2
+    for c in golden["decomposed_authored"]:
+        glob = program_from_json(c["program"])
+        local = program_from_json(c["local_program"])
+        dc = decomp_from_json(c["decomp"])
+        arrays = port.initial_fields(glob)
+        assert [fp_hex(a) for a in arrays] == c["init_fp"], c["name"]
+        lbs = [glob.field_bounds(i)[0] for i in range(glob.nfields)]
+        outs = port.simulate(local, dc, arrays, lbs, c["T"])
+        assert [fp_hex(a) for a in outs] == c["sim_fp"], c["name"]
+        assert c["sim_fp"] == c["serial_fp"] == c["mpi_sim_fp"]
+        assert isinstance(glob, hg.Program)

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--grid", default=None)
     ap.add_argument("--T", type=int, default=5)
     ap.add_argument("--calls", default=None, help="split T over several run calls, e.g. 2,3")
+    ap.add_argument("--golden", default=None,
+                    help="a decomposed_authored program of tests/golden (multi-apply)")
     a = ap.parse_args()
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -32,7 +34,15 @@ def main():
     torch.cuda.set_device(lr)
     dist.init_process_group("gloo")
     grid = [int(x) for x in a.grid.split("x")] if a.grid else [world] + [1] * (a.rank - 1)
-    prog = hg.build_kernel(hg.KernelSpec(a.kind, a.rank, a.extent, a.order, "f32"))
+    if a.golden:
+        import json
+        with open(os.path.join(REPO, "tests", "golden", "reference_golden.json")) as f:
+            (case,) = [c for c in json.load(f)["decomposed_authored"] if c["name"] == a.golden]
+        prog = hg.Program.from_json(case["program"])
+        a.rank = prog.rank
+        grid = [int(x) for x in a.grid.split("x")] if a.grid else case["grid"]
+    else:
+        prog = hg.build_kernel(hg.KernelSpec(a.kind, a.rank, a.extent, a.order, "f32"))
     local, dc = prog.decompose(grid)
     plan = hg.Plan(local, lr)
     coord = hg.coord_from_rank(rank, grid)
@@ -53,7 +63,7 @@ def main():
     glob = port.initial_fields(prog)
     lbs = [prog.field_bounds(i)[0] for i in range(prog.nfields)]
     want = port.simulate_rank_state(local, dc, glob, lbs, a.T, rank)
-    ok = all(np.array_equal(g.view(np.uint32), w.view(np.uint32)) for g, w in zip(got, want))
+    ok = all(np.array_equal(g.view(np.uint8), w.view(np.uint8)) for g, w in zip(got, want))
     flag = torch.tensor([0 if ok else 1])
     dist.all_reduce(flag)
     dist.barrier()
