@@ -6,6 +6,7 @@
 // __fadd_rn/__fmul_rn/... (never contracted) and this file is also built with -fmad=false.
 // Loads, schedules and data movement are free; operand pairing and evaluation order are not.
 #include "kernels.hpp"
+#include "device_util.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -72,90 +73,6 @@ int cudaErr(cudaError_t e, const char *what) {
   return setError(HG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// ---- exact arithmetic -----------------------------------------------------------------------
-__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
-__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
-
-template <typename T> __host__ __device__ inline T fromBits(uint64_t b);
-template <> __host__ __device__ inline float fromBits<float>(uint64_t b) {
-  uint32_t u = static_cast<uint32_t>(b);
-  float f;
-  memcpy(&f, &u, 4);
-  return f;
-}
-template <> __host__ __device__ inline double fromBits<double>(uint64_t b) {
-  double d;
-  memcpy(&d, &b, 8);
-  return d;
-}
-
-// ---- mbarrier / TMA PTX -------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smemAddr(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbarInit(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smemAddr(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbarExpectTx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemAddr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbarArrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smemAddr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbarWait(uint64_t *bar, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile("{\n\t.reg .pred p;\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}"
-                 : "=r"(done)
-                 : "r"(smemAddr(bar)), "r"(parity)
-                 : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tmaLoad3d(void *dst, const CUtensorMap *map, uint64_t *bar,
-                                          int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
-               "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smemAddr(dst)),
-               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
-               "r"(smemAddr(bar))
-               : "memory");
-}
-
-// Calls f(mb + U, integral_constant<U>) for U = 0, 1, ... while it returns true.
-template <typename F, int... Us>
-__device__ __forceinline__ void unrolled(F &f, int mb, std::integer_sequence<int, Us...>) {
-  (void)(f(mb + Us, std::integral_constant<int, Us>{}) && ...);
-}
-
-// 4 consecutive elements (16 B for f32, 2x16 B for f64) from 16-byte-aligned memory
-template <typename T> struct V4 { T v[4]; };
-__device__ __forceinline__ V4<float> ld4(const float *p) {
-  float4 t = *reinterpret_cast<const float4 *>(p);
-  return {{t.x, t.y, t.z, t.w}};
-}
-__device__ __forceinline__ V4<double> ld4(const double *p) {
-  double2 a = reinterpret_cast<const double2 *>(p)[0];
-  double2 b = reinterpret_cast<const double2 *>(p)[1];
-  return {{a.x, a.y, b.x, b.y}};
-}
-__device__ __forceinline__ void st4(float *p, const V4<float> &v) {
-  *reinterpret_cast<float4 *>(p) = make_float4(v.v[0], v.v[1], v.v[2], v.v[3]);
-}
-__device__ __forceinline__ void st4(double *p, const V4<double> &v) {
-  reinterpret_cast<double2 *>(p)[0] = make_double2(v.v[0], v.v[1]);
-  reinterpret_cast<double2 *>(p)[1] = make_double2(v.v[2], v.v[3]);
-}
-
 // ---- star family ------------------------------------------------------------------------
 //
 // One CTA owns a TX x TY tile of (x, y) columns and a chunk of z planes (dim 0).  A producer
@@ -203,20 +120,6 @@ template <typename T> struct StarParams {
   int boundary_last;
   T *out;
   T w0, wz[3], wy[3], wx[3], scale, two;
-};
-
-template <int NT> struct Taps;
-template <> struct Taps<1> {
-  static constexpr int R = 1;
-  __device__ static constexpr int k(int i) { return 1; }
-};
-template <> struct Taps<2> {
-  static constexpr int R = 2;
-  __device__ static constexpr int k(int i) { return i + 1; }
-};
-template <> struct Taps<3> {
-  static constexpr int R = 4;
-  __device__ static constexpr int k(int i) { return i == 0 ? 1 : (i == 1 ? 2 : 4); }
 };
 
 template <typename T, int RANK, int NT, int KIND> struct StarCfg {

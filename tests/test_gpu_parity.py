@@ -192,8 +192,7 @@ def test_simulate_multi_apply_matches_reference(golden, port):
         n = int(np.prod(c["grid"]))
         out = hg.simulate(glob, c["grid"], init, c["T"], devices=[0] * n)
         assert [fp_hex(b.data) for b in out] == c["sim_fp"], c["name"]
-        states = _sim_rank_states(glob, c["grid"], c["T"])
-        local, dc = glob.decompose(c["grid"])
+        local, dc, states = _sim_rank_states(glob, c["grid"], c["T"])
         arrays = port.initial_fields(glob)
         lbs = [glob.field_bounds(i)[0] for i in range(glob.nfields)]
         for rk in range(n):
