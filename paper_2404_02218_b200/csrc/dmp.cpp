@@ -158,6 +158,7 @@ int hg_dmp_create(hg_plan *plan, const hg_decomp *dc, int64_t rank, hg_dmp **out
     }
     if (rank < 0 || rank >= P)
       return setError(HG_EINVAL, "rank outside the process grid");
+    plan->tbOff = true; // peers address the buffers: no more buffer/shadow exchanges
     for (int s = 0; s < dc->nswaps; ++s) {
       if (dc->swaps[s].field < 0 || dc->swaps[s].field >= plan->prog.nfields)
         return setError(HG_EINVAL, "swap of a missing field");

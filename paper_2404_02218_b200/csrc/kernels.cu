@@ -890,22 +890,48 @@ __global__ void waitKernel(const unsigned long long *flags, int i0, int i1, int 
 
 // ---- host wrappers ---------------------------------------------------------------------------
 
-int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay, void *base,
-                       CUtensorMap *cur, CUtensorMap *prev) {
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensorMapEncoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   static std::once_flag once;
-  static int loadErr = 0;
   std::call_once(once, [&] {
     cudaDriverEntryPointQueryResult q;
     void *fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      loadErr = 1;
-    else
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   });
-  if (loadErr)
+  return encode;
+}
+} // namespace
+
+int makeBoxTensorMap(int dtype, const DevLayout &lay, void *base, const uint32_t box[3],
+                     CUtensorMap *out) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensorMapEncoder();
+  if (!encode)
+    return setError(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (lay.rank != 3)
+    return setError(HG_EINVAL, "box tensor maps are 3D");
+  const int es = dtype == HG_F32 ? 4 : 8;
+  cuuint64_t dims[3] = {cuuint64_t(lay.pitch), cuuint64_t(lay.shape[1]), cuuint64_t(lay.shape[0])};
+  cuuint64_t strides[2] = {cuuint64_t(lay.pitch * es), cuuint64_t(lay.pitch * lay.shape[1] * es)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  cuuint32_t bx[3] = {box[0], box[1], box[2]};
+  const CUtensorMapDataType dt =
+      dtype == HG_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  CUresult r = encode(out, dt, 3, base, dims, strides, bx, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return setError(HG_ECUDA, "cuTensorMapEncodeTiled(box) failed: " + std::to_string(int(r)));
+  return HG_OK;
+}
+
+int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay, void *base,
+                       CUtensorMap *cur, CUtensorMap *prev) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensorMapEncoder();
+  if (!encode)
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = dtype == HG_F32 ? 4 : 8;
   const int R = s.radius;

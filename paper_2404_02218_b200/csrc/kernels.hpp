@@ -54,6 +54,25 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
 int launchStar(StarLaunch &L, cudaStream_t st, int *blocks_out);
 int starResidentBlocks(const StarSpec &s, int dtype, int rank);
 
+// ---- two-step temporally blocked heat (tb.cu) --------------------------------------------
+struct TbLaunch {
+  const StarSpec *spec;
+  int dtype;
+  int64_t start[3], ext[3]; // core region, raw indices in the (shared) layout
+  DevLayout lay;
+  const CUtensorMap *tm_in; // input buffer, box from tbBox
+  void *mid;                // buffer of step t+1 (ring read; core written iff write_mid)
+  int write_mid;
+  void *out;                // buffer receiving step t+2
+  int chunks;               // z-chunks (0 = auto)
+};
+bool tbSupported(const StarSpec &s, int dtype, int rank);
+int tbBox(const StarSpec &s, int dtype, uint32_t box[3]);
+int launchTb(const TbLaunch &L, cudaStream_t st, int *blocks_out);
+// TMA descriptor of a whole 3D buffer with the given box (inner dimension first)
+int makeBoxTensorMap(int dtype, const DevLayout &lay, void *base, const uint32_t box[3],
+                     CUtensorMap *out);
+
 // ---- generic bytecode kernel ------------------------------------------------------------
 struct GenericLaunch {
   int dtype, rank;

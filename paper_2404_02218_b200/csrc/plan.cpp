@@ -461,6 +461,9 @@ int hg_plan_destroy(hg_plan *p) {
     cudaGraphExecDestroy(g.second);
   for (void *d : p->dptr)
     cudaFree(d);
+  for (void *d : p->shadow)
+    if (d)
+      cudaFree(d);
   for (void *d : p->tmpPtr)
     cudaFree(d);
   for (auto &m : p->multi)
@@ -478,6 +481,8 @@ int hg_plan_kernel_name(const hg_plan *p, char *name, size_t cap) {
                       ? p->an.name
                       : "generic" + std::to_string(p->prog.rank) + "d_" +
                             (p->prog.dtype == HG_F32 ? "f32" : "f64");
+  if (tbEligible(*p))
+    n += "+tb2"; // runs of >= 2 steps go through two-step passes (tb.cu)
   if (name && cap)
     std::snprintf(name, cap, "%s", n.c_str());
   return HG_OK;
@@ -504,6 +509,7 @@ int hg_plan_layout(const hg_plan *p, int b, hg_layout *out) {
 int hg_plan_init_fields(hg_plan *p, const int64_t *origin, void *stream) {
   if (!p)
     return setError(HG_EINVAL, "null plan");
+  std::fill(p->shadowOk.begin(), p->shadowOk.end(), 0);
   int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice");
   if (st)
     return st;
@@ -541,12 +547,128 @@ static int copy2d(hg_plan *p, int b, void *host, size_t bytes, void *stream, boo
 }
 
 int hg_plan_upload(hg_plan *p, int b, const void *host, size_t bytes, void *stream) {
+  if (p && b >= 0 && b < static_cast<int>(p->shadowOk.size()))
+    p->shadowOk[static_cast<size_t>(b)] = 0;
   return copy2d(p, b, const_cast<void *>(host), bytes, stream, true);
 }
 
 int hg_plan_download(hg_plan *p, int b, void *host, size_t bytes, void *stream) {
   return copy2d(p, b, host, bytes, stream, false);
 }
+
+} // extern "C"
+
+namespace hg {
+
+// Two-step passes (tb.cu) for large 3D heat steps on plans no dmp shares.  Opt-in
+// (HG_TB=1): bit-exact, but on B200 the FMA-free two-step pass is issue-bound below the
+// HBM-bound single step (profiles/r1_temporal_blocking.md), so it is not the default.
+bool tbEligible(const hg_plan &p) {
+  const char *on = std::getenv("HG_TB");
+  if (!on || on[0] != '1' || p.tbOff || p.an.family != Family::Star || !tbSupported(p.an.star, p.prog.dtype,
+                                                                   p.prog.rank))
+    return false;
+  int64_t pts = 1;
+  for (int d = 0; d < p.prog.rank; ++d)
+    pts *= p.an.dom_ub[d] - p.an.dom_lb[d];
+  return pts > (int64_t(1) << 22);
+}
+
+namespace {
+
+// Shadow of buffer b: same layout, same halo ring (a full copy once; the ring is never
+// written by a step, and the plan's own writers invalidate it).
+int ensureShadow(hg_plan &p, int b, cudaStream_t s) {
+  const size_t n = p.dptr.size();
+  if (p.shadow.size() != n) {
+    p.shadow.assign(n, nullptr);
+    p.shadowOk.assign(n, 0);
+    p.tmTb.resize(n);
+    p.tmTbSh.resize(n);
+    p.tmCurSh.resize(n);
+    p.tmPrevSh.resize(n);
+  }
+  const size_t bi = static_cast<size_t>(b);
+  const Layout &L = p.lay[bi];
+  uint32_t box[3];
+  tbBox(p.an.star, p.prog.dtype, box);
+  if (!p.shadow[bi]) {
+    int st = cudaCheck(cudaMalloc(&p.shadow[bi], L.bytes()), "cudaMalloc(shadow)");
+    if (st)
+      return st;
+    p.shadowOk[bi] = 0;
+    st = makeBoxTensorMap(p.prog.dtype, devLayout(L), p.dptr[bi], box, &p.tmTb[bi]);
+    if (!st)
+      st = makeBoxTensorMap(p.prog.dtype, devLayout(L), p.shadow[bi], box, &p.tmTbSh[bi]);
+    if (!st)
+      st = makeStarTensorMaps(p.an.star, p.prog.dtype, p.prog.rank, devLayout(L), p.shadow[bi],
+                              &p.tmCurSh[bi], &p.tmPrevSh[bi]);
+    if (st)
+      return st;
+  }
+  if (!p.shadowOk[bi]) {
+    int st = cudaCheck(cudaMemcpyAsync(p.shadow[bi], p.dptr[bi], L.bytes(),
+                                       cudaMemcpyDeviceToDevice, s),
+                       "shadow copy");
+    if (st)
+      return st;
+    p.shadowOk[bi] = 1;
+  }
+  return HG_OK;
+}
+
+void swapWithShadow(hg_plan &p, int b) {
+  const size_t bi = static_cast<size_t>(b);
+  std::swap(p.dptr[bi], p.shadow[bi]);
+  std::swap(p.tmTb[bi], p.tmTbSh[bi]);
+  std::swap(p.tmCur[bi], p.tmCurSh[bi]);
+  std::swap(p.tmPrev[bi], p.tmPrevSh[bi]);
+}
+
+// steps t+1, t+2 in one pass: reads the cur buffer, writes t+2 into its shadow (then the two
+// exchange), t+1 only into the ring-keeping output buffer when it must persist
+int tbPair(hg_plan &p, bool writeMid, cudaStream_t s) {
+  const hg_program &g = p.prog;
+  const StarSpec &sp = p.an.star;
+  const int bIn = p.bind[static_cast<size_t>(g.operand_field[sp.cur_operand])];
+  const int bMid = p.bind[static_cast<size_t>(g.store_field[0])];
+  int st = ensureShadow(p, bIn, s);
+  if (st)
+    return st;
+  TbLaunch L{};
+  L.spec = &sp;
+  L.dtype = g.dtype;
+  const Layout &lay = p.lay[static_cast<size_t>(bIn)];
+  for (int d = 0; d < 3; ++d) {
+    L.start[d] = g.store[0].lb[d] - lay.lb[d];
+    L.ext[d] = g.store[0].ub[d] - g.store[0].lb[d];
+  }
+  L.lay = devLayout(lay);
+  L.tm_in = &p.tmTb[static_cast<size_t>(bIn)];
+  L.mid = p.dptr[static_cast<size_t>(bMid)];
+  L.write_mid = writeMid ? 1 : 0;
+  L.out = p.shadow[static_cast<size_t>(bIn)];
+  L.chunks = 0;
+  st = launchTb(L, s, nullptr);
+  if (st)
+    return st;
+  swapWithShadow(p, bIn);
+  for (int k = 0; k < 2; ++k) { // the rotation of the two steps
+    std::vector<int> nxt(p.bind.size());
+    for (size_t i = 0; i < p.bind.size(); ++i)
+      nxt[i] = p.bind[static_cast<size_t>(p.an.src[i])];
+    p.bind.swap(nxt);
+  }
+  p.stepsDone += 2;
+  ++p.launches;
+  ++p.tbPasses;
+  return HG_OK;
+}
+
+} // namespace
+} // namespace hg
+
+extern "C" {
 
 int hg_plan_run(hg_plan *p, int64_t steps, void *stream) {
   if (!p)
@@ -557,6 +679,19 @@ int hg_plan_run(hg_plan *p, int64_t steps, void *stream) {
   if (st)
     return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (steps >= 2 && tbEligible(*p)) {
+    // pairs of steps; an odd step count ends with one ordinary step, which then also writes
+    // the t+1 buffer, so only an even count needs the last pair to store its t+1 core
+    const int64_t pairs = steps / 2;
+    for (int64_t k = 0; k < pairs; ++k) {
+      st = tbPair(*p, k + 1 == pairs && steps % 2 == 0, s);
+      if (st)
+        return st;
+    }
+    if (steps % 2)
+      return planStep(*p, s);
+    return HG_OK;
+  }
   // Launch-bound small grids (e.g. config 1, 1024^2 2D, ~2 us of work per step) replay a
   // CUDA graph of G consecutive steps captured once per binding phase: the launch sequence
   // repeats with the rotation period, and each node keeps its by-value parameters.
@@ -670,6 +805,8 @@ int hg_plan_pack(hg_plan *p, int b, const int64_t *at, const int64_t *size, void
 
 int hg_plan_unpack(hg_plan *p, int b, const int64_t *at, const int64_t *size, const void *src,
                    void *stream) {
+  if (p && b >= 0 && b < static_cast<int>(p->shadowOk.size()))
+    p->shadowOk[static_cast<size_t>(b)] = 0;
   return packImpl(p, b, at, size, const_cast<void *>(src), stream, 1);
 }
 

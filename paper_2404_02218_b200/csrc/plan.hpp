@@ -44,12 +44,21 @@ struct hg_plan {
     std::vector<int> resSlot;
   };
   std::vector<MultiApply> multi;
+  // two-step passes (tb.cu): per buffer a shadow allocation with the same halo ring, and the
+  // TMA descriptors of both; hg_plan_run exchanges a buffer with its shadow after each pass
+  std::vector<void *> shadow;
+  std::vector<char> shadowOk;         // ring of the shadow == ring of the buffer
+  std::vector<CUtensorMap> tmTb, tmTbSh, tmCurSh, tmPrevSh;
+  bool tbOff = false;                 // set once a dmp exported the buffers
+  int64_t tbPasses = 0;
 };
 
 namespace hg {
 int cudaCheck(cudaError_t e, const char *what);
 // One time step on `st` with the current binding, then rotate.
 int planStep(hg_plan &p, cudaStream_t st);
+// Whether hg_plan_run advances this plan by two-step passes (tb.cu).
+bool tbEligible(const hg_plan &p);
 } // namespace hg
 
 #endif

@@ -242,3 +242,68 @@ def test_rank_halos_bitwise_after_swaps(port, spec, grid, T):
         want = port.simulate_rank_state(local, dc, glob, lbs, T, rk)
         for g, w in zip(st, want):
             assert np.array_equal(g.view(np.uint32), w.view(np.uint32)), (spec, grid, rk)
+
+
+# ---- two-step passes (temporal blocking, tb.cu) ----------------------------------------------
+def _tb_case(port, prog, calls, upload_rng=None):
+    """Run `calls` (a list of step counts) through one plan and compare every buffer, halos
+    included, with the oracle; optionally upload random fields (rings included) first."""
+    plan = hg.Plan(prog)
+    plan.init_fields()
+    arrays = [plan.download(i) for i in range(prog.nfields)]
+    if upload_rng is not None:
+        plan.run(2)                 # make the plan own shadows, then replace the data
+        plan.reset_binding()
+        arrays = [upload_rng.random(a.shape, dtype=np.float32) for a in arrays]
+        for i, a in enumerate(arrays):
+            plan.upload(i, a)
+    l0 = plan.launch_count()
+    for c in calls:
+        plan.run(c)
+    launches = plan.launch_count() - l0
+    perm, _ = plan.binding()
+    got = [plan.download(p) for p in perm]
+    plan.close()
+    T = sum(calls)
+    perm_o = port.run(prog, arrays, T)
+    assert perm == perm_o
+    for g, o in zip(got, [arrays[p] for p in perm_o]):
+        assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
+    return launches
+
+
+@pytest.mark.parametrize("order,ext,calls", [
+    (4, [130, 200, 250], [4]), (4, [130, 200, 250], [5]), (4, [96, 160, 360], [3, 2, 1]),
+    (2, [100, 210, 243], [6]), (2, [171, 171, 171], [1, 4]), (4, [256, 64, 300], [2]),
+])
+def test_two_step_passes_bitwise(port, monkeypatch, order, ext, calls):
+    # heat 3D star, > 4M points: pairs of steps per pass, ragged tiles in x (not a multiple of
+    # the 120-point tile or of 4) and y, odd counts ending in one ordinary step, split calls
+    monkeypatch.setenv("HG_TB", "1")
+    prog = hg.build_kernel(hg.KernelSpec("heat", 3, 8, order, "f32")).with_extents(ext)
+    launches = _tb_case(port, prog, calls)
+    assert launches == sum(c // 2 + c % 2 for c in calls)
+
+
+def test_two_step_passes_after_upload(port, monkeypatch):
+    # uploads replace the rings too: the shadow of a buffer must follow
+    monkeypatch.setenv("HG_TB", "1")
+    prog = hg.build_kernel(hg.KernelSpec("heat", 3, 8, 4, "f32")).with_extents([140, 180, 200])
+    _tb_case(port, prog, [4, 3], upload_rng=np.random.default_rng(7))
+
+
+def test_two_step_matches_single_step(monkeypatch):
+    # the same run with passes disabled: identical buffers (and the same binding)
+    prog = hg.build_kernel(hg.KernelSpec("heat", 3, 176, 4, "f32"))
+    outs = []
+    for on in (True, False):
+        monkeypatch.setenv("HG_TB", "1" if on else "0")
+        plan = hg.Plan(prog)
+        plan.init_fields()
+        plan.run(6)
+        perm, _ = plan.binding()
+        outs.append((perm, [plan.download(p) for p in perm], plan.launch_count()))
+        plan.close()
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
