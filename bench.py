@@ -268,12 +268,14 @@ def run_ours(args):
     # (hg_plan_run) before the timed region
     steps(max(args.warmup, 40))
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     l0 = plan.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
+        # the barrier comes after every rank's sampler is live (nvidia-smi start-up varies by
+        # tens of ms): ranks whose halo neighbours start late would otherwise time the wait
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         ev0.record(stream)
         steps(args.steps)
         ev1.record(stream)

@@ -37,6 +37,9 @@
 #ifndef HG_MINB_R4
 #define HG_MINB_R4 1
 #endif
+#ifndef HG_MINB_R2
+#define HG_MINB_R2 3
+#endif
 #ifndef HG_TYT_R4
 #define HG_TYT_R4 16
 #endif
@@ -83,12 +86,18 @@ int cudaErr(cudaError_t e, const char *what) {
 // staged plane with 16-byte LDS.  Output planes are stored straight to HBM (STG.128).
 // Column-tile geometry: TXT x TYT consumer threads, 4 x-points each.  3D radius-4 tiles are
 // taller (more consumer warps in the single CTA an SM holds at ~110 registers).
-template <int RANK, int R> struct StarGeom;
-template <int R> struct StarGeom<3, R> {
+// GEO 1 is the wide tile (128 x 12, 2 CTAs/SM) chosen for large x-y planes (starGeoFor): its
+// smaller rim-to-core ratio cuts the halo re-reads of 1024^2 planes (sweep in
+// profiles/r1_sweeps.md); GEO 0 suits smaller planes.
+template <int RANK, int R, int GEO = 0> struct StarGeom;
+template <int R> struct StarGeom<3, R, 1> {
+  static constexpr int TXT = 32, TYT = 12;
+};
+template <int R> struct StarGeom<3, R, 0> {
   static constexpr int TXT = R >= 4 ? HG_TXT_R4 : HG_TXT_R2;
   static constexpr int TYT = R >= 4 ? HG_TYT_R4 : HG_TYT_R2;
 };
-template <int R> struct StarGeom<2, R> {
+template <int R> struct StarGeom<2, R, 0> {
   static constexpr int TXT = 32, TYT = 1;
 };
 
@@ -122,10 +131,10 @@ template <typename T> struct StarParams {
   T w0, wz[3], wy[3], wx[3], scale, two;
 };
 
-template <typename T, int RANK, int NT, int KIND> struct StarCfg {
+template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int R = Taps<NT>::R;
   static constexpr int RY = RANK == 3 ? R : 0;
-  static constexpr int TXT = StarGeom<RANK, R>::TXT, TYT = StarGeom<RANK, R>::TYT;
+  static constexpr int TXT = StarGeom<RANK, R, GEO>::TXT, TYT = StarGeom<RANK, R, GEO>::TYT;
   static constexpr int TX = TXT * 4, TY = TYT;
   static constexpr int PADX = 4;
   static constexpr int CW = TX + 2 * PADX;
@@ -134,7 +143,8 @@ template <typename T, int RANK, int NT, int KIND> struct StarCfg {
   static constexpr int NWARPS_C = NCONS / 32;
   static constexpr int NTHREADS = NCONS + 32;
   // CTAs per SM the register budget must allow (f32 3D: 3 for r<=2, 2 for r=4)
-  static constexpr int MINB = RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? 3 : HG_MINB_R4) : 1) : 4;
+  static constexpr int MINB =
+      GEO == 1 ? 2 : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
   static constexpr int DEPTH = RANK == 3 ? (R <= 2 ? HG_DEPTH3 : HG_DEPTH3W) : HG_DEPTH2;
   static constexpr int NS = R + 1 + DEPTH;
   static constexpr int Q = 2 * R + 1;
@@ -147,12 +157,12 @@ template <typename T, int RANK, int NT, int KIND> struct StarCfg {
       2 * NS * sizeof(uint64_t);
 };
 
-template <typename T, int RANK, int NT, int KIND>
-__global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND>::NTHREADS,
-                                  StarCfg<T, RANK, NT, KIND>::MINB)
+template <typename T, int RANK, int NT, int KIND, int GEO>
+__global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
+                                  StarCfg<T, RANK, NT, KIND, GEO>::MINB)
     starKernel(const __grid_constant__ CUtensorMap tmCur,
                const __grid_constant__ CUtensorMap tmPrev, const StarParams<T> P) {
-  using C = StarCfg<T, RANK, NT, KIND>;
+  using C = StarCfg<T, RANK, NT, KIND, GEO>;
   constexpr int R = C::R, RY = C::RY, NS = C::NS, Q = C::Q;
   extern __shared__ __align__(128) unsigned char smraw[];
   // align inside the __shared__ array (pointer stays in the shared window -> LDS, not LD)
@@ -456,10 +466,10 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND>::NTHREADS,
   }
 }
 
-template <typename T, int RANK, int NT, int KIND>
+template <typename T, int RANK, int NT, int KIND, int GEO = 0>
 int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
-  using C = StarCfg<T, RANK, NT, KIND>;
-  auto kern = starKernel<T, RANK, NT, KIND>;
+  using C = StarCfg<T, RANK, NT, KIND, GEO>;
+  auto kern = starKernel<T, RANK, NT, KIND, GEO>;
   // function attributes are per device: opt in to the large shared-memory carve-out on
   // every device this kernel is launched on
   static std::mutex mu;
@@ -610,7 +620,7 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
 
 template <typename T, int RANK, int NT, int KIND> int residentT() {
   using C = StarCfg<T, RANK, NT, KIND>;
-  auto kern = starKernel<T, RANK, NT, KIND>;
+  auto kern = starKernel<T, RANK, NT, KIND, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
   int per = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::NTHREADS, C::SMEM);
@@ -619,6 +629,12 @@ template <typename T, int RANK, int NT, int KIND> int residentT() {
 
 template <typename T, int RANK> int dispatchNT(StarLaunch &L, cudaStream_t st, int *b) {
   const StarSpec &s = *L.spec;
+  if constexpr (RANK == 3 && std::is_same_v<T, float>) {
+    if (L.geo == 1 && s.kind == kHeat && s.ntaps == 1)
+      return launchStarT<T, RANK, 1, kHeat, 1>(L, st, b);
+    if (L.geo == 1 && s.kind == kHeat && s.ntaps == 2)
+      return launchStarT<T, RANK, 2, kHeat, 1>(L, st, b);
+  }
   if (s.kind == kHeat) {
     if (s.ntaps == 1) return launchStarT<T, RANK, 1, kHeat>(L, st, b);
     if (s.ntaps == 2) return launchStarT<T, RANK, 2, kHeat>(L, st, b);
@@ -928,16 +944,29 @@ int makeBoxTensorMap(int dtype, const DevLayout &lay, void *base, const uint32_t
   return HG_OK;
 }
 
+int starGeoFor(const StarSpec &s, int dtype, int rank, const int64_t *ext) {
+  if (const char *e = std::getenv("HG_STAR_GEO")) // A/B experiments only
+    return std::atoi(e) == 1 && rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2;
+  // wide tiles pay on large planes (>= 768 x 768); 512^2 planes prefer the 64 x 16 tile
+  return rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2 && ext[1] >= 768 &&
+                 ext[2] >= 768
+             ? 1
+             : 0;
+}
+
 int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay, void *base,
-                       CUtensorMap *cur, CUtensorMap *prev) {
+                       CUtensorMap *cur, CUtensorMap *prev, int geo) {
   PFN_cuTensorMapEncodeTiled_v12000 encode = tensorMapEncoder();
   if (!encode)
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = dtype == HG_F32 ? 4 : 8;
   const int R = s.radius;
-  const int TX = (rank == 3 ? (R >= 4 ? StarGeom<3, 4>::TXT : StarGeom<3, 1>::TXT)
+  const int TX = (rank == 3 ? (geo == 1 ? StarGeom<3, 1, 1>::TXT
+                                        : R >= 4 ? StarGeom<3, 4>::TXT : StarGeom<3, 1>::TXT)
                             : StarGeom<2, 1>::TXT) * 4;
-  const int TY = rank == 3 ? (R >= 4 ? StarGeom<3, 4>::TYT : StarGeom<3, 1>::TYT) : 1;
+  const int TY = rank == 3 ? (geo == 1 ? StarGeom<3, 1, 1>::TYT
+                                       : R >= 4 ? StarGeom<3, 4>::TYT : StarGeom<3, 1>::TYT)
+                           : 1;
   const int RY = rank == 3 ? R : 0;
   cuuint64_t dims[3], strides[2];
   dims[0] = cuuint64_t(lay.pitch);

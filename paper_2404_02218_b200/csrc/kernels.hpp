@@ -35,6 +35,7 @@ struct StarLaunch {
   void *out;                  // base of the output buffer allocation
   int chunks;                 // z-chunks (0 = auto)
   int zorder_boundary_last;   // process z-boundary chunks last (dmp overlap)
+  int geo = 0;                // tile geometry (starGeoFor); the tensor maps must match
   const unsigned long long *wait_flags = nullptr; // dmp: my flag words (null = no wait)
   unsigned long long wait_epoch = 0;
   int wait_mask = 0;
@@ -50,7 +51,9 @@ struct StarLaunch {
 };
 // Creates the TMA descriptor of a buffer for the star family's cur/prev boxes.
 int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay,
-                       void *base, CUtensorMap *cur, CUtensorMap *prev);
+                       void *base, CUtensorMap *cur, CUtensorMap *prev, int geo);
+// Tile geometry of the star kernel for a core of extents ext (dims 0..rank-1).
+int starGeoFor(const StarSpec &s, int dtype, int rank, const int64_t *ext);
 int launchStar(StarLaunch &L, cudaStream_t st, int *blocks_out);
 int starResidentBlocks(const StarSpec &s, int dtype, int rank);
 

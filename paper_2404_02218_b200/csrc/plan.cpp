@@ -252,6 +252,7 @@ int planStep(hg_plan &p, cudaStream_t st) {
     L.tm_prev = &p.tmPrev[static_cast<size_t>(bPrev)];
     L.out = p.dptr[static_cast<size_t>(bOut)];
     L.chunks = p.chunks;
+    L.geo = p.starGeo;
     L.zorder_boundary_last = p.boundaryLast;
     L.wait_flags = p.waitFlags;
     L.wait_epoch = p.waitEpoch;
@@ -409,12 +410,16 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
   if (p->an.family == Family::Star && p->an.star.kind == kCopy)
     p->an.family = Family::Generic; // a plain copy needs no stencil machinery
   if (p->an.family == Family::Star) {
+    int64_t ext[3] = {0, 0, 0};
+    for (int d = 0; d < g.rank; ++d)
+      ext[d] = g.store[0].ub[d] - g.store[0].lb[d];
+    p->starGeo = starGeoFor(p->an.star, g.dtype, g.rank, ext);
     p->tmCur.resize(static_cast<size_t>(g.nfields));
     p->tmPrev.resize(static_cast<size_t>(g.nfields));
     for (int f = 0; f < g.nfields; ++f) {
       st = makeStarTensorMaps(p->an.star, g.dtype, g.rank, devLayout(p->lay[static_cast<size_t>(f)]),
                               p->dptr[static_cast<size_t>(f)], &p->tmCur[static_cast<size_t>(f)],
-                              &p->tmPrev[static_cast<size_t>(f)]);
+                              &p->tmPrev[static_cast<size_t>(f)], p->starGeo);
       if (st)
         return st;
     }
@@ -602,7 +607,7 @@ int ensureShadow(hg_plan &p, int b, cudaStream_t s) {
       st = makeBoxTensorMap(p.prog.dtype, devLayout(L), p.shadow[bi], box, &p.tmTbSh[bi]);
     if (!st)
       st = makeStarTensorMaps(p.an.star, p.prog.dtype, p.prog.rank, devLayout(L), p.shadow[bi],
-                              &p.tmCurSh[bi], &p.tmPrevSh[bi]);
+                              &p.tmCurSh[bi], &p.tmPrevSh[bi], p.starGeo);
     if (st)
       return st;
   }

@@ -24,6 +24,7 @@ struct hg_plan {
   std::vector<int> resSlot;
   int64_t launches = 0;
   int chunks = 0;                     // star z-chunks (0 = auto)
+  int starGeo = 0;                    // star tile geometry (starGeoFor)
   int boundaryLast = 0;               // star: z-boundary chunks last (dmp overlap)
   // one-shot (consumed by the next planStep): halo faces the star kernel must wait for
   const unsigned long long *waitFlags = nullptr;

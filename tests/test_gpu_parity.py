@@ -307,3 +307,31 @@ def test_two_step_matches_single_step(monkeypatch):
     assert outs[0][0] == outs[1][0]
     for a, b in zip(outs[0][1], outs[1][1]):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+# ---- wide-tile geometry of the star kernel (large x-y planes) ---------------------------------
+@pytest.mark.parametrize("order,ext,T", [(4, [36, 800, 1000], 3), (2, [20, 771, 903], 4)])
+def test_wide_tile_geometry_bitwise(port, order, ext, T):
+    # planes >= 768 x 768 take the 128 x 12 tile (starGeoFor); ragged in x and y
+    prog = hg.build_kernel(hg.KernelSpec("heat", 3, 8, order, "f32")).with_extents(ext)
+    arrays = port.initial_fields(prog)
+    perm_o = port.run(prog, arrays, T)
+    _, fin, perm, _ = _plan_run(prog, T)
+    assert perm == perm_o
+    for g, o in zip(fin, [arrays[p] for p in perm_o]):
+        assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
+@pytest.mark.parametrize("spec,grid,T", [(("heat", 3, 24, 4), [2, 2, 1], 4),
+                                         (("heat", 3, 32, 2), [1, 2, 2], 3)])
+def test_wide_tile_rank_halos(port, monkeypatch, spec, grid, T):
+    # the wide tile forced on small ranks: per-rank halos after device swaps stay bitwise
+    monkeypatch.setenv("HG_STAR_GEO", "1")
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    local, dc, states = _sim_rank_states(prog, grid, T)
+    glob = port.initial_fields(prog)
+    lbs = [prog.field_bounds(i)[0] for i in range(prog.nfields)]
+    for rk in range(int(np.prod(grid))):
+        want = port.simulate_rank_state(local, dc, glob, lbs, T, rk)
+        for g, o in zip(states[rk], want):
+            assert np.array_equal(g.view(np.uint32), o.view(np.uint32)), rk

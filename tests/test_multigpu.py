@@ -48,6 +48,23 @@ def test_ipc_dmp_two_ranks(args):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("grid", ["2x1x1", "1x2x2", "2x2x1"])
+def test_ipc_dmp_wide_tile(grid):
+    # the wide star tile (forced) with the fused next-step swap over NVLink
+    n = _ngpus()
+    nproc = int(np.prod([int(x) for x in grid.split("x")]))
+    if n < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node",
+           str(nproc), os.path.join(REPO, "tools", "dmp_check.py"), "--kind", "heat", "--rank",
+           "3", "--extent", "64", "--order", "4", "--T", "6", "--calls", "2,4", "--grid", grid]
+    r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, HG_STAR_GEO="1"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name,grids", [("indep2f_2d", ["2x1", "1x2", "2x2"]),
                                         ("twin3_3d_f64", ["2x1x1", "1x1x2", "2x2x1"])])
 def test_ipc_dmp_multi_apply(name, grids):
