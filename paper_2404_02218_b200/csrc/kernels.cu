@@ -23,7 +23,7 @@
 #define HG_DEPTH3 5
 #endif
 #ifndef HG_DEPTH3W
-#define HG_DEPTH3W 5
+#define HG_DEPTH3W 7
 #endif
 #ifndef HG_DEPTH2
 #define HG_DEPTH2 4
@@ -41,7 +41,7 @@
 #define HG_MINB_R2 3
 #endif
 #ifndef HG_TYT_R4
-#define HG_TYT_R4 16
+#define HG_TYT_R4 24
 #endif
 #ifndef HG_TXT_R4
 #define HG_TXT_R4 16
