@@ -58,8 +58,9 @@ def _peaks():
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, wait: bool = True):
         self.device = device
+        self.wait = wait
         self.proc = None
         self.lines = []
 
@@ -75,7 +76,7 @@ class ClockSampler:
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
             t0 = time.time()  # the timed region starts only once sampling is live
-            while not self.lines and time.time() - t0 < 10:
+            while self.wait and not self.lines and time.time() - t0 < 10:
                 time.sleep(0.02)
         except Exception:
             self.proc = None
@@ -266,13 +267,36 @@ def run_ours(args):
     core_local = local.core_points()
     # warm-up: W steps, and at least 40 so that launch-bound configs capture their CUDA graph
     # (hg_plan_run) before the timed region
+    torch.cuda.synchronize()
+    tw = time.perf_counter()
     steps(max(args.warmup, 40))
     torch.cuda.synchronize()
+    per_step = (time.perf_counter() - tw) / max(args.warmup, 40)
     l0 = plan.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
-        # the barrier comes after every rank's sampler is live (nvidia-smi start-up varies by
-        # tens of ms): ranks whose halo neighbours start late would otherwise time the wait
+    with ClockSampler(local_rank, wait=False) as clk:
+        # Keep the GPU busy until every rank's nvidia-smi sampler is live (its start-up takes
+        # 0.1-1 s and varies by rank): an idle GPU drops its clocks, which short timed regions
+        # then measure, and ranks entering the timed region apart time their neighbours' late
+        # halos.  Chunks of >= ~20 ms of steps; all ranks run the same chunks (MIN-reduce).
+        chunk = max(1, min(2000, int(0.02 / max(per_step, 1e-7)) + 1))
+        if world > 1:  # every rank must run the same steps (the halo swaps pair them up)
+            c = torch.tensor([chunk], dtype=torch.int32, device=dev)
+            dist.all_reduce(c, op=dist.ReduceOp.MAX)
+            chunk = int(c.item())
+        t0 = time.perf_counter()
+        while True:
+            steps(chunk)
+            torch.cuda.synchronize()
+            ready = 1 if (clk.lines and time.perf_counter() - t0 > 0.2) else 0
+            if time.perf_counter() - t0 > 15:
+                ready = 1
+            if world > 1:
+                r = torch.tensor([ready], dtype=torch.int32, device=dev)
+                dist.all_reduce(r, op=dist.ReduceOp.MIN)
+                ready = int(r.item())
+            if ready:
+                break
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
