@@ -272,7 +272,6 @@ def run_ours(args):
     steps(max(args.warmup, 40))
     torch.cuda.synchronize()
     per_step = (time.perf_counter() - tw) / max(args.warmup, 40)
-    l0 = plan.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank, wait=False) as clk:
         # Keep the GPU busy until every rank's nvidia-smi sampler is live (its start-up takes
@@ -300,6 +299,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        l0 = plan.launch_count()
         ev0.record(stream)
         steps(args.steps)
         ev1.record(stream)
