@@ -69,7 +69,12 @@ def single_apply(seed: int):
     fb = _btxt([-h] * r, [x + h for x in n])
     ftype = f"!field<{fb}x{elem}>"
     args = [f"%in{i} : {ftype}" for i in range(nin)] + [f"%out{i} : {ftype}" for i in range(nout)]
-    L = [f"builtin.module {{", f"  func.func @step({', '.join(args)}) {{"]
+    # time slots: output i replaces input i next step (ping-pong groups, kernels.cpp:139-243)
+    slots = ""
+    if rng.random() < 0.5:
+        groups = [f"[{i}, {nin + i}]" for i in range(min(nin, nout))]
+        slots = f" attributes {{stencil.time_slots = [{', '.join(groups)}]}}"
+    L = [f"builtin.module{slots} {{", f"  func.func @step({', '.join(args)}) {{"]
     for i in range(nin):
         L.append(f"    %t{i} = stencil.load %in{i} : {ftype} -> !temp<?x{elem}>")
     names = [f"%a{i}" for i in range(nin)]

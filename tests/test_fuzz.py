@@ -12,8 +12,9 @@ from helpers import fp_hex, prog_to_json
 import randprog
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SINGLE = list(range(30))
-MULTI = list(range(100, 115))
+SINGLE = list(range(60))
+MULTI = list(range(100, 130))
+T = 3
 
 
 def _texts():
@@ -23,7 +24,7 @@ def _texts():
 
 @pytest.fixture(scope="module")
 def printed(ref):
-    """Each random module after the reference's parser + propagate-bounds, and its T=2 run."""
+    """Each random module after the reference's parser + propagate-bounds, and its T-step run."""
     sys.path.insert(0, os.path.join(HERE, "golden"))
     from make_golden import prog_json
     out = []
@@ -32,7 +33,7 @@ def printed(ref):
         mod = ref.pipeline(ref.parse(text), "propagate-bounds")
         prog, ops, _ = ref.export_program(mod)
         init = L.hr_initial_fields(mod)
-        fin = L.hr_run_serial(mod, L.hr_bufs_clone(init), 2)
+        fin = L.hr_run_serial(mod, L.hr_bufs_clone(init), T)
         assert fin, ref.err()
         fps = ["%016x" % L.hr_fingerprint(fin, i) for i in range(L.hr_bufs_count(fin))]
         out.append((kind, seed, ref.print(mod), prog_json(prog, ops), fps))
@@ -44,7 +45,7 @@ def test_random_modules_reader_and_oracle_match_reference(printed, port):
         prog, _, _ = hg.Program.parse(text)
         assert prog_to_json(prog) == pj, (kind, seed)
         arrays = port.initial_fields(prog)
-        perm = port.run(prog, arrays, 2)
+        perm = port.run(prog, arrays, T)
         assert [fp_hex(arrays[p]) for p in perm] == fps, (kind, seed)
 
 
@@ -64,13 +65,13 @@ def test_random_modules_on_gpu(printed, port, monkeypatch, family):
         prog, _, _ = hg.Program.parse(text)
         plan = hg.Plan(prog)
         plan.init_fields()
-        plan.run(2)
+        plan.run(T)
         perm, _ = plan.binding()
         got = [plan.download(p) for p in perm]
         seen.add(plan.kernel_name.split("_")[0])
         plan.close()
         arrays = port.initial_fields(prog)
-        perm_o = port.run(prog, arrays, 2)
+        perm_o = port.run(prog, arrays, T)
         assert perm == perm_o
         for i, (g, o) in enumerate(zip(got, [arrays[p] for p in perm_o])):
             assert _same(g, o), (kind, seed, i, plan.kernel_name)
