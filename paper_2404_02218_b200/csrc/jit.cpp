@@ -109,6 +109,13 @@ std::string constLiteral(uint64_t bits, int dtype) {
 
 } // namespace
 
+int jitMisaligned(const hg_program &p, const Layout &lay) {
+  const int r = p.rank, es = p.dtype == HG_F32 ? 4 : 8;
+  const long long col = lay.col0 + (p.store[0].lb[r - 1] - lay.lb[r - 1]);
+  const int v = 16 / es;
+  return int(((col % v) + v) % v);
+}
+
 bool jitEligible(const hg_program &p, const Analysis &a, std::string *why) {
   auto no = [&](const char *m) {
     if (why)
@@ -281,9 +288,6 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
         s << "    const V4 " << nm << "c" << c << " = ld4(" << base << " + " << (c - 1) * 4
           << ");\n";
   }
-  s << "    __syncwarp();\n"
-       "    if (lane == 0) mb_arrive(&empty[sOld]);\n"
-       "    if (++sOld == NS) sOld = 0;\n";
   // the DAG, 4 points
   for (int k = 0; k < p.nresults; ++k)
     s << "    V4 res" << k << ";\n";
@@ -322,6 +326,13 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
       s << "      res" << k << ".v[" << j << "] = v" << p.result_op[k] << ";\n";
     s << "    }\n";
   }
+  // release plane m's stage only once every value read from it has been consumed: with two
+  // 16-byte loads per f64 window, releasing right after issuing the loads let the producer's
+  // next TMA land in the stage before the second load had read it (wrong f64 values when a
+  // dz = -1 window and a dy = -1 window coincide; tests/test_gpu_parity.py jit_f64 case)
+  s << "    __syncwarp();\n"
+       "    if (lane == 0) mb_arrive(&empty[sOld]);\n"
+       "    if (++sOld == NS) sOld = 0;\n";
   s << "    if (yok) {\n"
        "      const long long e = obase + (long long)m * P.plane;\n";
   for (int k = 0; k < p.nresults; ++k)
@@ -448,6 +459,13 @@ int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
   int nz = int(p.store[0].ub[0] - p.store[0].lb[0]);
   int ny = r == 3 ? int(p.store[0].ub[1] - p.store[0].lb[1]) : 1;
   int nx = int(p.store[0].ub[r - 1] - p.store[0].lb[r - 1]);
+  // the kernel's 16-byte row vectors need an aligned first column: a region starting off the
+  // layout's aligned core column (a multi-apply producer widened below in x) is evaluated
+  // from the aligned column below it; the extra columns land in the temp outside its domain,
+  // which no consumer reads (jitMisaligned: such applies never write a field directly)
+  const int mis = jitMisaligned(p, lay);
+  xs -= mis;
+  nx += mis;
   int tiles_x = (nx + K.tx - 1) / K.tx, tiles_y = (ny + K.ty - 1) / K.ty;
   // z-chunks of ~32 planes (measured best for the PW set: 4 chunks at nz=128)
   int nch = chunks > 0 ? chunks : std::max(1, (nz + 16) / 32);

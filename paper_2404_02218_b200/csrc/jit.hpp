@@ -22,6 +22,8 @@ struct JitKernel {
 };
 
 bool jitEligible(const hg_program &p, const Analysis &a, std::string *why);
+// Columns by which the first column of p's store region sits above a 16-byte boundary of lay.
+int jitMisaligned(const hg_program &p, const Layout &lay);
 int jitBuildSource(const hg_program &p, JitKernel &K);    // codegen
 int jitCompile(JitKernel &K);                              // NVRTC -> sm_100a cubin
 int jitLoad(JitKernel &K, int device);                    // current device

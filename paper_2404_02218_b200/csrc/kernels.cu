@@ -89,15 +89,17 @@ int cudaErr(cudaError_t e, const char *what) {
 // GEO 1 is the wide tile (128 x 12, 2 CTAs/SM) chosen for large x-y planes (starGeoFor): its
 // smaller rim-to-core ratio cuts the halo re-reads of 1024^2 planes (sweep in
 // profiles/r1_sweeps.md); GEO 0 suits smaller planes.
-template <int RANK, int R, int GEO = 0> struct StarGeom;
-template <int R> struct StarGeom<3, R, 1> {
+// f64 radius-4 stars keep the 64 x 16 tile and a depth-5 ring (the taller f32 tile's ring
+// would exceed the 227 KB of shared memory at 8 bytes per element).
+template <int RANK, int R, int GEO = 0, int ES = 4> struct StarGeom;
+template <int R, int ES> struct StarGeom<3, R, 1, ES> {
   static constexpr int TXT = 32, TYT = 12;
 };
-template <int R> struct StarGeom<3, R, 0> {
+template <int R, int ES> struct StarGeom<3, R, 0, ES> {
   static constexpr int TXT = R >= 4 ? HG_TXT_R4 : HG_TXT_R2;
-  static constexpr int TYT = R >= 4 ? HG_TYT_R4 : HG_TYT_R2;
+  static constexpr int TYT = R >= 4 ? (ES == 8 ? 16 : HG_TYT_R4) : HG_TYT_R2;
 };
-template <int R> struct StarGeom<2, R, 0> {
+template <int R, int ES> struct StarGeom<2, R, 0, ES> {
   static constexpr int TXT = 32, TYT = 1;
 };
 
@@ -134,7 +136,8 @@ template <typename T> struct StarParams {
 template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int R = Taps<NT>::R;
   static constexpr int RY = RANK == 3 ? R : 0;
-  static constexpr int TXT = StarGeom<RANK, R, GEO>::TXT, TYT = StarGeom<RANK, R, GEO>::TYT;
+  static constexpr int TXT = StarGeom<RANK, R, GEO, int(sizeof(T))>::TXT,
+                       TYT = StarGeom<RANK, R, GEO, int(sizeof(T))>::TYT;
   static constexpr int TX = TXT * 4, TY = TYT;
   static constexpr int PADX = 4;
   static constexpr int CW = TX + 2 * PADX;
@@ -145,7 +148,8 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   // CTAs per SM the register budget must allow (f32 3D: 3 for r<=2, 2 for r=4)
   static constexpr int MINB =
       GEO == 1 ? 2 : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
-  static constexpr int DEPTH = RANK == 3 ? (R <= 2 ? HG_DEPTH3 : HG_DEPTH3W) : HG_DEPTH2;
+  static constexpr int DEPTH =
+      RANK == 3 ? (R <= 2 ? HG_DEPTH3 : (sizeof(T) == 8 ? 5 : HG_DEPTH3W)) : HG_DEPTH2;
   static constexpr int NS = R + 1 + DEPTH;
   static constexpr int Q = 2 * R + 1;
   static constexpr int STAGE = ROWS * CW;   // elements
@@ -287,8 +291,6 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       q[i][j] = c.v[j];
-    if (i < R)
-      release(s);
   }
 
   const bool yok = RANK == 2 || (yb + ty < P.ny);
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     V4<T> pv;
     if constexpr (C::WAVE)
       pv = ld4(pstages + size_t(sC) * C::PSTAGE + ty * C::TX + x0);
-    release(sC);
+    const int sDone = sC;
     if (++sC == NS)
       sC = 0;
 
@@ -382,6 +384,16 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         o.v[j] = add_(sub_(mul_(c, P.two), pv.v[j]), mul_(acc, P.scale));
       else
         o.v[j] = add_(c, mul_(acc, P.scale));
+    }
+    // Release a stage only after the values read from it are consumed: an arrive right after
+    // issuing the LDS let the producer's next TMA land in the stage before a load had read it
+    // (observed with f64 windows in the generated kernels).  Planes 0..R-1 fed only the queue
+    // and go with the first output plane.
+    release(sDone);
+    if (m == 0) {
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        release(i % NS);
     }
     if (yok) {
       T *dst = outRow + int64_t(m) * P.plane;
@@ -961,11 +973,14 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const int es = dtype == HG_F32 ? 4 : 8;
   const int R = s.radius;
+  const bool f64 = dtype != HG_F32;
   const int TX = (rank == 3 ? (geo == 1 ? StarGeom<3, 1, 1>::TXT
                                         : R >= 4 ? StarGeom<3, 4>::TXT : StarGeom<3, 1>::TXT)
                             : StarGeom<2, 1>::TXT) * 4;
   const int TY = rank == 3 ? (geo == 1 ? StarGeom<3, 1, 1>::TYT
-                                       : R >= 4 ? StarGeom<3, 4>::TYT : StarGeom<3, 1>::TYT)
+                                       : R >= 4 ? (f64 ? StarGeom<3, 4, 0, 8>::TYT
+                                                       : StarGeom<3, 4>::TYT)
+                                                : StarGeom<3, 1>::TYT)
                            : 1;
   const int RY = rank == 3 ? R : 0;
   cuuint64_t dims[3], strides[2];

@@ -127,10 +127,115 @@ int compileGeneric(hg_plan &p) {
   return uploadOps(out, &p.gopsDev);
 }
 
+// Multi-apply through the fused-apply family: every apply becomes a single-apply program over
+// virtual fields [fields..., temps...] that all share the field layout, compiled to generated
+// straight-line code.  A result no later apply reads and exactly one store copies over the
+// apply's whole domain is written straight into that field (no temp, no copy).  Returns
+// false (nothing allocated) when some apply does not fit the family.
+bool sameBox(const hg_bounds &a, const hg_bounds &b, int rank) {
+  for (int d = 0; d < rank; ++d)
+    if (a.lb[d] != b.lb[d] || a.ub[d] != b.ub[d])
+      return false;
+  return true;
+}
+
+bool compileMultiJit(hg_plan &p, int device, int &st) {
+  st = HG_OK;
+  const hg_program &g = p.prog;
+  const int F = g.nfields;
+  if (std::getenv("HG_NO_APPLY_JIT") || F + g.ntemps > HG_MAX_FIELDS || g.rank < 2)
+    return false;
+  for (int f = 1; f < F; ++f)
+    for (int d = 0; d < g.rank; ++d)
+      if (g.fields[f].lb[d] != g.fields[0].lb[d] || g.fields[f].ub[d] != g.fields[0].ub[d])
+        return false;
+  std::vector<int> consumers(static_cast<size_t>(g.ntemps), 0), stores(static_cast<size_t>(g.ntemps), 0);
+  for (int a = 0; a < g.napplies; ++a)
+    for (int o = 0; o < p.applies[static_cast<size_t>(a)].noperands; ++o)
+      if (p.applies[static_cast<size_t>(a)].operand[o] < 0)
+        ++consumers[static_cast<size_t>(-p.applies[static_cast<size_t>(a)].operand[o] - 1)];
+  for (int k = 0; k < g.nstores; ++k)
+    ++stores[static_cast<size_t>(g.mstore_temp[k])];
+  std::vector<hg_plan::MultiApply> ms(static_cast<size_t>(g.napplies));
+  p.storeDone.assign(static_cast<size_t>(g.nstores), 0);
+  for (int a = 0; a < g.napplies; ++a) {
+    const hg_apply &A = p.applies[static_cast<size_t>(a)];
+    hg_plan::MultiApply &M = ms[static_cast<size_t>(a)];
+    hg_program &S = M.sub;
+    std::memset(&S, 0, sizeof S);
+    S.rank = g.rank;
+    S.dtype = g.dtype;
+    S.nfields = F + g.ntemps;
+    for (int i = 0; i < S.nfields; ++i)
+      S.fields[i] = g.fields[0];
+    S.noperands = A.noperands;
+    for (int o = 0; o < A.noperands; ++o)
+      S.operand_field[o] = A.operand[o] >= 0 ? A.operand[o] : F + (-A.operand[o] - 1);
+    S.nops = A.nops;
+    S.ops = p.ops.data() + A.op_begin;
+    S.nresults = A.nresults;
+    M.direct.assign(static_cast<size_t>(A.nresults), -1);
+    for (int k = 0; k < A.nresults; ++k) {
+      const int t = A.result_temp[k];
+      S.result_op[k] = A.result_op[k];
+      S.store_field[k] = F + t;
+      S.store[k] = A.domain;
+      if (consumers[static_cast<size_t>(t)] == 0 && stores[static_cast<size_t>(t)] == 1 &&
+          !std::getenv("HG_MULTI_NODIRECT") && jitMisaligned(S, p.lay[0]) == 0)
+        for (int j = 0; j < g.nstores; ++j)
+          if (g.mstore_temp[j] == t && sameBox(g.mstore[j], A.domain, g.rank)) {
+            M.direct[static_cast<size_t>(k)] = g.mstore_field[j];
+            p.storeDone[static_cast<size_t>(j)] = 1;
+          }
+    }
+    Analysis none;
+    if (!jitEligible(S, none, nullptr))
+      return false;
+    M.jit = jitCached(S, device);
+    if (!M.jit)
+      return false;
+  }
+  // temps in the field layout (only the ones some apply or store still reads)
+  p.tmpLay.assign(static_cast<size_t>(g.ntemps), p.lay[0]);
+  p.tmpPtr.assign(static_cast<size_t>(g.ntemps), nullptr);
+  for (int t = 0; t < g.ntemps; ++t) {
+    if (!consumers[static_cast<size_t>(t)] && !stores[static_cast<size_t>(t)])
+      continue;
+    st = cudaCheck(cudaMalloc(&p.tmpPtr[static_cast<size_t>(t)], p.lay[0].bytes()),
+                   "cudaMalloc(temp)");
+    if (st)
+      return true;
+    cudaMemset(p.tmpPtr[static_cast<size_t>(t)], 0, p.lay[0].bytes());
+  }
+  for (auto &M : ms) {
+    M.tmField.resize(static_cast<size_t>(F));
+    M.tmTemp.resize(static_cast<size_t>(g.ntemps));
+    for (int f = 0; f < F && !st; ++f)
+      st = jitTensorMap(*M.jit, g.dtype, g.rank, p.lay[static_cast<size_t>(f)],
+                        p.dptr[static_cast<size_t>(f)], &M.tmField[static_cast<size_t>(f)]);
+    for (int t = 0; t < g.ntemps && !st; ++t)
+      if (p.tmpPtr[static_cast<size_t>(t)])
+        st = jitTensorMap(*M.jit, g.dtype, g.rank, p.lay[0], p.tmpPtr[static_cast<size_t>(t)],
+                          &M.tmTemp[static_cast<size_t>(t)]);
+    if (st)
+      return true;
+  }
+  p.multi = std::move(ms);
+  p.an.name = "multi" + std::to_string(g.napplies) + "x_apply" + std::to_string(g.rank) + "d_" +
+              (g.dtype == HG_F32 ? "f32" : "f64");
+  return true;
+}
+
 // Multi-apply: one compiled slice per apply, temps in HBM laid out over their domains.
 int compileMulti(hg_plan &p) {
   const hg_program &g = p.prog;
   const int es = g.dtype == HG_F32 ? 4 : 8;
+  {
+    int st = HG_OK;
+    if (compileMultiJit(p, p.device, st))
+      return st;
+  }
+  p.storeDone.assign(static_cast<size_t>(g.nstores), 0);
   p.tmpLay.assign(static_cast<size_t>(g.ntemps), Layout{});
   p.tmpPtr.assign(static_cast<size_t>(g.ntemps), nullptr);
   for (int a = 0; a < g.napplies; ++a) {
@@ -172,6 +277,24 @@ int multiStep(hg_plan &p, cudaStream_t st) {
   for (int a = 0; a < g.napplies; ++a) {
     const hg_apply &A = p.applies[static_cast<size_t>(a)];
     const hg_plan::MultiApply &M = p.multi[static_cast<size_t>(a)];
+    if (M.jit) {
+      const CUtensorMap *tms[HG_MAX_FIELDS];
+      void *outs[HG_MAX_RESULTS];
+      for (int o = 0; o < A.noperands; ++o)
+        tms[o] = A.operand[o] >= 0
+                     ? &M.tmField[static_cast<size_t>(p.bind[static_cast<size_t>(A.operand[o])])]
+                     : &M.tmTemp[static_cast<size_t>(-A.operand[o] - 1)];
+      for (int k = 0; k < A.nresults; ++k) {
+        const int f = M.direct[static_cast<size_t>(k)];
+        outs[k] = f >= 0 ? p.dptr[static_cast<size_t>(p.bind[static_cast<size_t>(f)])]
+                         : p.tmpPtr[static_cast<size_t>(A.result_temp[k])];
+      }
+      int rc = jitLaunch(*M.jit, M.sub, p.lay[0], tms, outs, 0, st);
+      if (rc)
+        return rc;
+      ++p.launches;
+      continue;
+    }
     GenericLaunch L{};
     L.dtype = g.dtype;
     L.rank = g.rank;
@@ -211,6 +334,8 @@ int multiStep(hg_plan &p, cudaStream_t st) {
     ++p.launches;
   }
   for (int k = 0; k < g.nstores; ++k) { // stencil.store: temp region -> field
+    if (p.storeDone[static_cast<size_t>(k)])
+      continue;
     const int t = g.mstore_temp[k];
     const int b = p.bind[static_cast<size_t>(g.mstore_field[k])];
     int rc = launchCopyBox(p.tmpPtr[static_cast<size_t>(t)], devLayout(p.tmpLay[static_cast<size_t>(t)]),

@@ -43,8 +43,15 @@ struct hg_plan {
     hg::GOp *ops = nullptr;
     int nslots = 0;
     std::vector<int> resSlot;
+    // fused-apply form: the apply as a single-apply program over virtual fields
+    // [fields..., temps...] (all in the field layout), its generated kernel, TMA descriptors
+    std::shared_ptr<hg::JitKernel> jit;
+    hg_program sub{};
+    std::vector<CUtensorMap> tmField, tmTemp;
+    std::vector<int> direct; // per result: field written in place of the temp, or -1
   };
   std::vector<MultiApply> multi;
+  std::vector<char> storeDone; // multi-apply stores folded into their apply (direct results)
   // two-step passes (tb.cu): per buffer a shadow allocation with the same halo ring, and the
   // TMA descriptors of both; hg_plan_run exchanges a buffer with its shadow after each pass
   std::vector<void *> shadow;

@@ -267,6 +267,10 @@ from paper_2404_02218_b200.programs.pw_advection import xir as pw_xir  # noqa: E
 
 AUTHORED["pw_advection_16x24x40"] = pw_xir(16, 24, 40)
 AUTHORED["pw_advection_f64_9x10x11"] = pw_xir(9, 10, 11, "f64")
+from paper_2404_02218_b200.programs.flux3d import xir as flux_xir  # noqa: E402
+
+AUTHORED["flux3d_12x10x21"] = flux_xir(12, 10, 21)
+AUTHORED["flux3d_f64_7x9x8"] = flux_xir(7, 9, 8, "f64")
 
 SERIAL = [  # (kind, rank, extent, order, f32, T)
     ("heat", 1, 16, 2, 1, 5), ("heat", 1, 128, 8, 0, 7),

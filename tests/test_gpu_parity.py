@@ -335,3 +335,20 @@ def test_wide_tile_rank_halos(port, monkeypatch, spec, grid, T):
         want = port.simulate_rank_state(local, dc, glob, lbs, T, rk)
         for g, o in zip(states[rk], want):
             assert np.array_equal(g.view(np.uint32), o.view(np.uint32)), rk
+
+
+@pytest.mark.parametrize("family", ["apply", "generic"])
+def test_multi_apply_flux3d_medium(port, monkeypatch, family):
+    # the authored two-stage flux step (apply consuming apply) at a medium ragged size, through
+    # the per-apply fused kernels (consumer result stored in place) and the generic kernel
+    from paper_2404_02218_b200.programs.flux3d import xir
+    if family == "generic":
+        monkeypatch.setenv("HG_NO_APPLY_JIT", "1")
+    prog, _, _ = hg.Program.parse(xir(70, 130, 203))
+    arrays = port.initial_fields(prog)
+    perm_o = port.run(prog, arrays, 3)
+    _, fin, perm, name = _plan_run(prog, 3)
+    assert name.startswith("multi2x_" + ("apply" if family == "apply" else "generic")), name
+    assert perm == perm_o
+    for g, o in zip(fin, [arrays[p] for p in perm_o]):
+        assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
