@@ -215,6 +215,12 @@ int hg_parse_program(const char *text, hg_program *prog, hg_op *ops, int cap_ops
  * ("star3d_r2_heat", "generic", ...) into name[cap]. No GPU needed. */
 int hg_program_match(const hg_program *prog, char *name, size_t cap);
 
+/* Apply fusion: a multi-apply step as one single-apply program (temps inlined: each temp
+ * access becomes the producer's DAG at the shifted point, memoised per (apply, shift)).
+ * Bit-identical to materialising the temps.  HG_EUNSUPPORTED when the inlined DAG would
+ * exceed the op budget or leave the field bounds. */
+int hg_fuse_applies(const hg_program *prog, hg_program *out, hg_op *ops, int cap_ops);
+
 /* The fused-apply family (generated straight-line code for any apply DAG): generate the
  * kernel source for `prog` and compile it with NVRTC for sm_100a, without a GPU.  Writes the
  * generated CUDA source into src[cap] (may be NULL) and the cubin size into *cubin_bytes. */

@@ -268,6 +268,13 @@ class Program:
             at += n
         return out
 
+    def fuse_applies(self) -> "Program":
+        """The multi-apply step as one single-apply program (hg_fuse_applies)."""
+        ops = (HgOp * capi.HG_MAX_OPS)()
+        out = HgProgram()
+        check(lib().hg_fuse_applies(C.byref(self.prog), C.byref(out), ops, capi.HG_MAX_OPS))
+        return Program(out, ops)
+
     def store_region(self, k: int = 0):
         """Stored region k (hg_bounds) of either program form."""
         return self.prog.mstore[k] if self.prog.napplies > 0 else self.prog.store[k]

@@ -115,6 +115,7 @@ def lib() -> C.CDLL:
                                               P(HgProgram), P(HgOp), C.c_int]),
         "hg_program_match": (C.c_int, [P(HgProgram), C.c_char_p, SZ]),
         "hg_apply_compile": (C.c_int, [P(HgProgram), C.c_char_p, SZ, P(SZ)]),
+        "hg_fuse_applies": (C.c_int, [P(HgProgram), P(HgProgram), P(HgOp), C.c_int]),
         "hg_parse_program": (C.c_int, [C.c_char_p, P(HgProgram), P(HgOp), C.c_int, P(HgApply),
                                        C.c_int, P(HgDecomp), P(C.c_int), C.c_char_p, SZ]),
         "hg_decompose_program": (C.c_int, [P(HgProgram), C.c_int, P(I64), P(HgProgram),

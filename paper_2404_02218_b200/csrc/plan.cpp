@@ -489,6 +489,23 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
   int st = analyze(p->prog, p->an);
   if (st)
     return st;
+  // a multi-apply step runs as one fused single-apply program when its temps inline within
+  // the op budget (hg_fuse_applies); else apply by apply through HBM temps
+  if (p->prog.napplies > 0 && !std::getenv("HG_NO_FUSE_APPLIES")) {
+    std::vector<hg_op> fops(HG_MAX_OPS);
+    hg_program fused;
+    if (hg_fuse_applies(&p->prog, &fused, fops.data(), HG_MAX_OPS) == HG_OK) {
+      fops.resize(static_cast<size_t>(fused.nops));
+      p->namePrefix = "multi" + std::to_string(p->prog.napplies) + "x_fused_";
+      p->ops = std::move(fops);
+      p->prog = fused;
+      p->prog.ops = p->ops.data();
+      p->applies.clear();
+      st = analyze(p->prog, p->an);
+      if (st)
+        return st;
+    }
+  }
   const hg_program &g = p->prog;
   // rotating buffers must share one layout (the kernel addresses a slot, not a buffer)
   {
@@ -607,10 +624,10 @@ int hg_plan_destroy(hg_plan *p) {
 int hg_plan_kernel_name(const hg_plan *p, char *name, size_t cap) {
   if (!p)
     return setError(HG_EINVAL, "null plan");
-  std::string n = p->an.family != Family::Generic
-                      ? p->an.name
-                      : "generic" + std::to_string(p->prog.rank) + "d_" +
-                            (p->prog.dtype == HG_F32 ? "f32" : "f64");
+  std::string n = p->namePrefix + (p->an.family != Family::Generic
+                                      ? p->an.name
+                                      : "generic" + std::to_string(p->prog.rank) + "d_" +
+                                            (p->prog.dtype == HG_F32 ? "f32" : "f64"));
   if (tbEligible(*p))
     n += "+tb2"; // runs of >= 2 steps go through two-step passes (tb.cu)
   if (name && cap)

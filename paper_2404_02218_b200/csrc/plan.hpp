@@ -6,6 +6,7 @@
 #include "kernels.hpp"
 
 #include <map>
+#include <string>
 #include <memory>
 #include <vector>
 
@@ -58,6 +59,7 @@ struct hg_plan {
   std::vector<char> shadowOk;         // ring of the shadow == ring of the buffer
   std::vector<CUtensorMap> tmTb, tmTbSh, tmCurSh, tmPrevSh;
   bool tbOff = false;                 // set once a dmp exported the buffers
+  std::string namePrefix;             // "multiNx_fused_" when the applies were fused
   int64_t tbPasses = 0;
 };
 

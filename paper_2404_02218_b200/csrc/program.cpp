@@ -4,10 +4,14 @@
 // under /root/reference/proj/core.
 #include "hg_internal.hpp"
 
+#include <algorithm>
+#include <array>
 #include <charconv>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <numeric>
 #include <string>
 
@@ -803,6 +807,138 @@ int hg_build_kernel_program(const char *kind_c, int rank, int64_t extent, int or
   p.group_len[0] = numFields;
   for (int f = 0; f < numFields; ++f)
     p.groups[f] = f;
+  return HG_OK;
+}
+
+// ---- apply fusion: a multi-apply step as one single-apply program ------------------------
+//
+// Every temp access of a stored apply is replaced by the producing apply's DAG evaluated at the
+// shifted point (recursively), so the fused program reads fields only.  Each inlined value is
+// computed by the same IEEE ops, in the same order, from the same inputs as the reference's
+// materialised temp at that point (interpreter.cpp:713-758), hence bit-identical; propagate-
+// bounds already guaranteed that every such point lies inside the producer's domain.  The
+// (apply, shift) pairs are memoised, so a temp read at k distinct offsets costs k copies of its
+// producer -- cheap next to the HBM round trip of a materialised temp.
+int hg_fuse_applies(const hg_program *prog, hg_program *out, hg_op *ops, int cap_ops) {
+  if (!prog || !out || !ops)
+    return setError(HG_EINVAL, "null argument");
+  const hg_program &g = *prog;
+  if (g.napplies <= 0)
+    return setError(HG_EINVAL, "not a multi-apply program");
+  int st = validateProgram(g);
+  if (st)
+    return st;
+  const int r = g.rank;
+  std::vector<int> defApply(static_cast<size_t>(g.ntemps), -1), defResult(static_cast<size_t>(g.ntemps), -1);
+  for (int a = 0; a < g.napplies; ++a)
+    for (int k = 0; k < g.applies[a].nresults; ++k) {
+      defApply[static_cast<size_t>(g.applies[a].result_temp[k])] = a;
+      defResult[static_cast<size_t>(g.applies[a].result_temp[k])] = k;
+    }
+  std::vector<hg_op> outOps;
+  std::vector<int> fieldOperand(static_cast<size_t>(g.nfields), -1); // field -> fused operand
+  int nopnd = 0;
+  // fields in load order, keeping only those some inlined access reads (assigned lazily)
+  auto operandOf = [&](int f) {
+    if (fieldOperand[static_cast<size_t>(f)] < 0)
+      fieldOperand[static_cast<size_t>(f)] = nopnd++;
+    return fieldOperand[static_cast<size_t>(f)];
+  };
+  const size_t budget = static_cast<size_t>(std::min<int64_t>(HG_MAX_OPS, std::max(64, 16 * g.nops)));
+  std::map<std::pair<int, std::array<int64_t, 3>>, std::vector<int>> memo;
+  bool overflow = false;
+  std::function<const std::vector<int> &(int, std::array<int64_t, 3>)> inl =
+      [&](int a, std::array<int64_t, 3> sh) -> const std::vector<int> & {
+    auto key = std::make_pair(a, sh);
+    auto it = memo.find(key);
+    if (it != memo.end())
+      return it->second;
+    const hg_apply &A = g.applies[a];
+    std::vector<int> map(static_cast<size_t>(A.nops), 0);
+    for (int i = 0; i < A.nops && !overflow; ++i) {
+      const hg_op &o = g.ops[A.op_begin + i];
+      hg_op h;
+      std::memset(&h, 0, sizeof h);
+      if (o.code == HG_OP_ACCESS) {
+        std::array<int64_t, 3> off = {0, 0, 0};
+        for (int d = 0; d < r; ++d)
+          off[static_cast<size_t>(d)] = o.off[d] + sh[static_cast<size_t>(d)];
+        const int x = A.operand[o.operand];
+        if (x < 0) { // a temp: its producer's value at the shifted point
+          const int t = -x - 1;
+          const std::vector<int> &pm = inl(defApply[static_cast<size_t>(t)], off);
+          if (overflow)
+            break;
+          const hg_apply &P = g.applies[defApply[static_cast<size_t>(t)]];
+          map[static_cast<size_t>(i)] = pm[static_cast<size_t>(P.result_op[defResult[static_cast<size_t>(t)]])];
+          continue;
+        }
+        h.code = HG_OP_ACCESS;
+        h.operand = operandOf(x);
+        for (int d = 0; d < r; ++d)
+          h.off[d] = off[static_cast<size_t>(d)];
+      } else if (o.code == HG_OP_CONST) {
+        h = o;
+      } else {
+        h.code = o.code;
+        h.a = map[static_cast<size_t>(o.a)];
+        h.b = map[static_cast<size_t>(o.b)];
+      }
+      if (outOps.size() >= budget) {
+        overflow = true;
+        break;
+      }
+      map[static_cast<size_t>(i)] = static_cast<int>(outOps.size());
+      outOps.push_back(h);
+    }
+    return memo.emplace(key, std::move(map)).first->second;
+  };
+  hg_program f = g;
+  f.napplies = 0;
+  f.applies = nullptr;
+  f.ntemps = 0;
+  f.nstores = 0;
+  if (g.nstores > HG_MAX_RESULTS)
+    return setError(HG_EUNSUPPORTED, "apply fusion: more stores than results of one apply");
+  f.nresults = g.nstores;
+  for (int k = 0; k < g.nstores; ++k) {
+    const int t = g.mstore_temp[k];
+    const std::vector<int> &m = inl(defApply[static_cast<size_t>(t)], {0, 0, 0});
+    if (overflow)
+      return setError(HG_EUNSUPPORTED, "apply fusion: inlined DAG exceeds the op budget");
+    const hg_apply &P = g.applies[defApply[static_cast<size_t>(t)]];
+    f.result_op[k] = m[static_cast<size_t>(P.result_op[defResult[static_cast<size_t>(t)]])];
+    f.store_field[k] = g.mstore_field[k];
+    f.store[k] = g.mstore[k];
+  }
+  // operands: the accessed fields in load order
+  std::vector<int> order;
+  for (int o = 0; o < g.noperands; ++o)
+    if (fieldOperand[static_cast<size_t>(g.operand_field[o])] >= 0 &&
+        std::find(order.begin(), order.end(), g.operand_field[o]) == order.end())
+      order.push_back(g.operand_field[o]);
+  for (int fi = 0; fi < g.nfields; ++fi) // accessed but not in the load list (hand-built)
+    if (fieldOperand[static_cast<size_t>(fi)] >= 0 &&
+        std::find(order.begin(), order.end(), fi) == order.end())
+      order.push_back(fi);
+  std::vector<int> remap(static_cast<size_t>(nopnd), 0);
+  for (size_t i = 0; i < order.size(); ++i)
+    remap[static_cast<size_t>(fieldOperand[static_cast<size_t>(order[i])])] = static_cast<int>(i);
+  for (auto &h : outOps)
+    if (h.code == HG_OP_ACCESS)
+      h.operand = remap[static_cast<size_t>(h.operand)];
+  f.noperands = static_cast<int>(order.size());
+  for (size_t i = 0; i < order.size(); ++i)
+    f.operand_field[i] = order[i];
+  if (static_cast<int>(outOps.size()) > cap_ops)
+    return setError(HG_EINVAL, "op buffer too small");
+  std::copy(outOps.begin(), outOps.end(), ops);
+  f.nops = static_cast<int>(outOps.size());
+  f.ops = ops;
+  st = validateProgram(f);
+  if (st)
+    return setError(HG_EUNSUPPORTED, std::string("apply fusion: ") + hg_last_error());
+  *out = f;
   return HG_OK;
 }
 

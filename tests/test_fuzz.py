@@ -49,6 +49,22 @@ def test_random_modules_reader_and_oracle_match_reference(printed, port):
         assert [fp_hex(arrays[p]) for p in perm] == fps, (kind, seed)
 
 
+def test_random_multi_apply_fusion_on_oracle(printed, port):
+    # hg_fuse_applies (temps inlined) == the materialised multi-apply step, on the oracle
+    n = 0
+    for kind, seed, text, _, fps in printed:
+        if kind != "multi":
+            continue
+        prog, _, _ = hg.Program.parse(text)
+        fused = prog.fuse_applies()
+        assert fused.prog.napplies == 0
+        arrays = port.initial_fields(fused)
+        perm = port.run(fused, arrays, T)
+        assert [fp_hex(arrays[p]) for p in perm] == fps, seed
+        n += 1
+    assert n >= 20
+
+
 def _same(a, b):
     ua = a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
     ub = b.view(np.uint32 if b.dtype == np.float32 else np.uint64)
@@ -56,10 +72,12 @@ def _same(a, b):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("family", ["default", "generic"])
+@pytest.mark.parametrize("family", ["default", "generic", "unfused"])
 def test_random_modules_on_gpu(printed, port, monkeypatch, family):
     if family == "generic":
         monkeypatch.setenv("HG_NO_APPLY_JIT", "1")
+    if family == "unfused":
+        monkeypatch.setenv("HG_NO_FUSE_APPLIES", "1")
     seen = set()
     for kind, seed, text, _, _ in printed:
         prog, _, _ = hg.Program.parse(text)

@@ -52,16 +52,20 @@ def test_config1_full_run_bitwise(golden):
     assert [fp_hex(a) for a in fin] == ["b11e8dddf9e8c23c", "34a5556efc0dfea0"]
 
 
-@pytest.mark.parametrize("family", ["apply", "generic"])
+@pytest.mark.parametrize("family", ["apply", "generic", "unfused"])
 def test_authored_programs_bitwise(golden, monkeypatch, family):
     # multi-operand / multi-result / divide / diagonal programs incl. the authored
-    # PW-advection set: the fused-apply family (NVRTC-generated) and the generic kernel
+    # PW-advection set: the fused-apply family (NVRTC-generated) and the generic kernel;
+    # multi-apply steps fused (default) or apply by apply ("unfused")
     if family == "generic":
         monkeypatch.setenv("HG_NO_APPLY_JIT", "1")
+    if family == "unfused":
+        monkeypatch.setenv("HG_NO_FUSE_APPLIES", "1")
     for c in golden["authored"]:
         prog = program_from_json(c["program"])
         init, fin, _, name = _plan_run(prog, c["T"])
         want = ("multi" if "applies" in c["program"] else
+                "apply" if family == "unfused" and prog.rank >= 2 else
                 family if prog.rank >= 2 else "generic")
         assert name.startswith(want), (c["name"], name)
         assert [fp_hex(a) for a in init] == c["init_fp"], c["name"]
@@ -337,18 +341,23 @@ def test_wide_tile_rank_halos(port, monkeypatch, spec, grid, T):
             assert np.array_equal(g.view(np.uint32), o.view(np.uint32)), rk
 
 
-@pytest.mark.parametrize("family", ["apply", "generic"])
-def test_multi_apply_flux3d_medium(port, monkeypatch, family):
-    # the authored two-stage flux step (apply consuming apply) at a medium ragged size, through
-    # the per-apply fused kernels (consumer result stored in place) and the generic kernel
+@pytest.mark.parametrize("family,prefix", [
+    ("fused", "multi2x_fused_apply3d"), ("unfused", "multi2x_apply3d"),
+    ("generic", "multi2x_generic3d"), ("fused_generic", "multi2x_fused_generic3d")])
+def test_multi_apply_flux3d_medium(port, monkeypatch, family, prefix):
+    # the authored two-stage flux step (apply consuming apply) at a medium ragged size: fused
+    # into one generated kernel (temps inlined), apply by apply through HBM temps (consumer
+    # stored in place), and both on the generic kernel
     from paper_2404_02218_b200.programs.flux3d import xir
-    if family == "generic":
+    if family in ("unfused", "generic"):
+        monkeypatch.setenv("HG_NO_FUSE_APPLIES", "1")
+    if family in ("generic", "fused_generic"):
         monkeypatch.setenv("HG_NO_APPLY_JIT", "1")
     prog, _, _ = hg.Program.parse(xir(70, 130, 203))
     arrays = port.initial_fields(prog)
     perm_o = port.run(prog, arrays, 3)
     _, fin, perm, name = _plan_run(prog, 3)
-    assert name.startswith("multi2x_" + ("apply" if family == "apply" else "generic")), name
+    assert name.startswith(prefix), name
     assert perm == perm_o
     for g, o in zip(fin, [arrays[p] for p in perm_o]):
         assert np.array_equal(g.view(np.uint32), o.view(np.uint32))

@@ -143,3 +143,18 @@ def test_decomposed_multi_apply(golden, port):
         assert [fp_hex(a) for a in outs] == c["sim_fp"], c["name"]
         assert c["sim_fp"] == c["serial_fp"] == c["mpi_sim_fp"]
         assert isinstance(glob, hg.Program)
+
+
+def test_apply_fusion_matches_reference(golden, port):
+    # hg_fuse_applies: every authored multi-apply step fused into one apply reproduces the
+    # reference's materialised run bit for bit (on the oracle)
+    n = 0
+    for c in golden["authored"]:
+        if "applies" not in c["program"]:
+            continue
+        fused = program_from_json(c["program"]).fuse_applies()
+        arrays = port.initial_fields(fused)
+        perm = port.run(fused, arrays, c["T"])
+        assert [fp_hex(arrays[p]) for p in perm] == c["final_fp"], c["name"]
+        n += 1
+    assert n >= 5

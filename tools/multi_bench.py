@@ -26,8 +26,7 @@ print(plan.kernel_name, "%%.1f GPts/s" %% (n ** 3 * T / ms / 1e6), "(8 B/pt idea
 if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
     T = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-    for off in ("1", ""):
-        env = dict(os.environ)
-        if off:
-            env["HG_NO_APPLY_JIT"] = "1"
+    for flags in ({"HG_NO_FUSE_APPLIES": "1", "HG_NO_APPLY_JIT": "1"},
+                  {"HG_NO_FUSE_APPLIES": "1"}, {}):
+        env = dict(os.environ, **flags)
         subprocess.run([sys.executable, "-c", CHILD % (REPO, n, T)], env=env, check=True)
