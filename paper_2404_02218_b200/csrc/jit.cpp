@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -177,11 +178,22 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   const int ve = 128 / es;
   const int stage = rows * cw;
   const int sstride = (stage + ve - 1) / ve * ve;
-  const int depth = 3;
+  // TMA planes in flight beyond the 2RZ+1 window: 6 where shared memory allows (PW set:
+  // 214 -> 224 GPts/s from depth 3 to 6, profiles/r1_sweeps.md), down to 1
+  static const int want = [] {
+    const char *e = std::getenv("HG_JIT_DEPTH"); // tuning experiments only
+    return e ? std::max(1, std::atoi(e)) : 6;
+  }();
+  auto smemFor = [&](int d) {
+    return 128 + static_cast<size_t>(es) * (2 * rz + 1 + d) * O * sstride + 2 * (2 * rz + 1 + d) * 8;
+  };
+  int depth = want;
+  while (depth > 1 && smemFor(depth) > 227 * 1024)
+    --depth;
   K.ns = 2 * rz + 1 + depth;
   K.ncons = K.txt * K.tyt;
   K.nthreads = K.ncons + 32;
-  K.smem = 128 + static_cast<size_t>(es) * K.ns * O * sstride + 2 * K.ns * 8;
+  K.smem = smemFor(depth);
   if (K.smem > 227 * 1024)
     return setError(HG_EUNSUPPORTED, "fused apply family: shared-memory ring too large");
   const std::string T = tname(p.dtype);
