@@ -252,14 +252,19 @@ def run_ours(args):
         local, dc, origin = wl["build"](hg), None, None
     plan = hg.Plan(local, local_rank)
     plan.init_fields(origin=origin, stream=sh)
-    dmp = None
+    dmp = nccl = None
     if world > 1 and dc is not None:
-        dmp = hg.Dmp(plan, dc, rank)
-        hd.connect(dmp, rank, grid, world)
+        if args.transport == "nccl":   # the comparison baseline, not the product path
+            nccl = hd.NcclSwap(plan, dc, rank, grid, stream=sh)
+        else:
+            dmp = hg.Dmp(plan, dc, rank)
+            hd.connect(dmp, rank, grid, world)
         dist.barrier()
 
     def steps(k):
-        if dmp is None:
+        if nccl is not None:
+            nccl.run(k)
+        elif dmp is None:
             plan.run(k, stream=sh)
         else:
             dmp.run(k, stream=sh)
@@ -388,7 +393,9 @@ def run_ours(args):
                        "core_per_gpu": list(dc.core[:3]) if dc is not None else None,
                        "global_core": gext, "grid": grid, "halo": 2,
                        "l2": "inputs >> 126 MB L2 (GBs of fields per GPU), no flush needed",
-                       "transport": "NVLink P2P put (CUDA IPC) + system-scope flags"
+                       "transport": ("NCCL send/recv of packed boxes (baseline)"
+                                     if args.transport == "nccl" else
+                                     "NVLink P2P put (CUDA IPC) + system-scope flags")
                        if world > 1 else "none"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -419,6 +426,9 @@ def main():
     ap.add_argument("--grid", default=None, help="process grid AxBxC (default: weak N x 1 x 1, "
                                                  "strong 1/2x1x1/2x2x1/2x2x2)")
     ap.add_argument("--mode", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="halo transport at N>1: p2p = the product (fused NVLink puts), "
+                         "nccl = packed boxes over NCCL send/recv (comparison baseline)")
     ap.add_argument("--workload", default="heat3d_weak", choices=list(WORKLOADS))
     ap.add_argument("--strong-extent", type=int, default=2048)
     ap.add_argument("--e2e-timesteps", type=int, default=100)

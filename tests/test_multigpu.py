@@ -48,6 +48,28 @@ def test_ipc_dmp_two_ranks(args):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("args", [
+    ["--kind", "heat", "--rank", "3", "--extent", "48", "--order", "4", "--T", "5"],
+    ["--kind", "wave", "--rank", "3", "--extent", "40", "--order", "8", "--T", "4",
+     "--calls", "1,3"],
+])
+def test_nccl_transport_baseline(args):
+    # the NCCL comparison transport (dist.NcclSwap) is bit-exact too, halos included
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    for nproc, grid in ((2, "2x1x1"), (4, "2x2x1")):
+        if nproc > n:
+            continue
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone",
+               "--nproc-per-node", str(nproc), os.path.join(REPO, "tools", "dmp_check.py"),
+               "--transport", "nccl", "--grid", grid] + args
+        r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("grid", ["2x1x1", "1x2x2", "2x2x1"])
 def test_ipc_dmp_wide_tile(grid):
     # the wide star tile (forced) with the fused next-step swap over NVLink

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--grid", default=None)
     ap.add_argument("--T", type=int, default=5)
     ap.add_argument("--calls", default=None, help="split T over several run calls, e.g. 2,3")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="p2p: hg_dmp (fused NVLink puts); nccl: the packed-box NCCL baseline")
     ap.add_argument("--golden", default=None,
                     help="a decomposed_authored program of tests/golden (multi-apply)")
     a = ap.parse_args()
@@ -32,7 +34,10 @@ def main():
     rank = int(os.environ["RANK"])
     lr = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr)
-    dist.init_process_group("gloo")
+    if a.transport == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    else:
+        dist.init_process_group("gloo")
     grid = [int(x) for x in a.grid.split("x")] if a.grid else [world] + [1] * (a.rank - 1)
     if a.golden:
         import json
@@ -47,9 +52,12 @@ def main():
     plan = hg.Plan(local, lr)
     coord = hg.coord_from_rank(rank, grid)
     plan.init_fields(origin=[coord[d] * dc.core[d] for d in range(a.rank)])
-    dmp = hg.Dmp(plan, dc, rank)
     from paper_2404_02218_b200 import dist as hd
-    hd.connect(dmp, rank, grid, world)
+    if a.transport == "nccl":
+        dmp = hd.NcclSwap(plan, dc, rank, grid)
+    else:
+        dmp = hg.Dmp(plan, dc, rank)
+        hd.connect(dmp, rank, grid, world)
     dist.barrier()
     calls = [int(x) for x in a.calls.split(",")] if a.calls else [a.T]
     assert sum(calls) == a.T
@@ -64,10 +72,11 @@ def main():
     lbs = [prog.field_bounds(i)[0] for i in range(prog.nfields)]
     want = port.simulate_rank_state(local, dc, glob, lbs, a.T, rank)
     ok = all(np.array_equal(g.view(np.uint8), w.view(np.uint8)) for g, w in zip(got, want))
-    flag = torch.tensor([0 if ok else 1])
+    flag = torch.tensor([0 if ok else 1], device="cuda" if a.transport == "nccl" else "cpu")
     dist.all_reduce(flag)
     dist.barrier()
-    dmp.close()
+    if a.transport != "nccl":
+        dmp.close()
     plan.close()
     if rank == 0:
         print(f"dmp_check {a.kind}{a.rank}d n{a.extent} o{a.order} grid={grid} T={a.T}: "
