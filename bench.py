@@ -168,6 +168,27 @@ def cpu_baseline(workload="heat3d_weak"):
             "seconds": secs}
 
 
+def dead_on_arrival_bytes(prog, es):
+    """Bytes hg_plan_upload_live skips with the initial binding: the store box of every slot
+    the step stores into (one store) without loading it (mirrors plan.cpp)."""
+    p = prog.prog
+    loaded = {p.operand_field[o] for o in range(p.noperands)}
+    if p.napplies:
+        stores = [(p.mstore_field[k], p.mstore[k]) for k in range(p.nstores)]
+    else:
+        stores = [(p.store_field[k], p.store[k]) for k in range(p.nresults)]
+    total = 0
+    for f in range(p.nfields):
+        boxes = [b for g, b in stores if g == f]
+        if f in loaded or len(boxes) != 1:
+            continue
+        n = 1
+        for d in range(p.rank):
+            n *= boxes[0].ub[d] - boxes[0].lb[d]
+        total += n * es
+    return total
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU implementation, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
@@ -344,13 +365,15 @@ def run_ours(args):
                                     pin_memory=True))
         for i in range(local.nfields):  # the synthetic inputs live on the host
             plan.download(i, host[i].numpy(), stream=sh)
-        h2d = sum(h.numel() * 4 for h in host)
-        d2h = h2d
+        # bytes moved per call: every field down; every field up except the store box of a
+        # slot the first step overwrites before reading it (hg_plan_upload_live)
+        d2h = sum(h.numel() * 4 for h in host)
+        h2d = d2h - dead_on_arrival_bytes(local, 4)
 
         def e2e_call():
-            for i in range(local.nfields):
-                plan.upload(i, host[i].numpy(), stream=sh)
             plan.reset_binding()
+            for i in range(local.nfields):
+                plan.upload(i, host[i].numpy(), stream=sh, live=True)
             if dmp is not None:
                 dmp.invalidate()
             steps(T)
@@ -373,8 +396,10 @@ def run_ours(args):
         secs = float(el.item())
         e2e = {"value": core_local * world * T * n_calls / secs / 1e9, "unit": "GPts/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "step": f"one runSerialStencil-style call: upload fields from pinned host, "
-                       f"{T} time steps, download the final binding (per rank)",
+               "step": f"one runSerialStencil-style call: upload fields from pinned host "
+                       f"(zero-copy kernel; the output slot's core, overwritten unread by "
+                       f"step 1, is not moved), {T} time steps, download the final binding "
+                       f"(per rank)",
                "calls": n_calls}
 
     if rank == 0:

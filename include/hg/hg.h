@@ -244,8 +244,17 @@ int hg_plan_layout(const hg_plan *plan, int buffer, hg_layout *out);
  * origin may be NULL (zeros).  The decomposed form passes the rank's core offset. */
 int hg_plan_init_fields(hg_plan *plan, const int64_t *origin, void *stream);
 /* Host <-> device copy of buffer `buffer` (initial argument index) in the reference's
- * row-major packed layout; bytes must equal the buffer's logical size. */
+ * row-major packed layout; bytes must equal the buffer's logical size.  Pinned (device-mapped)
+ * host memory moves in one zero-copy kernel pass at the flat PCIe rate; pageable memory goes
+ * through the copy engines.  Uploads are asynchronous on `stream`; downloads return when the
+ * bytes are on the host. */
 int hg_plan_upload(hg_plan *plan, int buffer, const void *host, size_t bytes, void *stream);
+/* hg_plan_upload minus the region the next step overwrites before anything reads it: when the
+ * slot `buffer` is bound to is stored into (one store) and not loaded by the step, its store
+ * box is not moved (runSerialStencil's output slot: the core of u_out, the reference's fresh
+ * apply result copied over it at step 1, interpreter.cpp:683-712).  The caller must run at
+ * least one step before reading the buffer back. */
+int hg_plan_upload_live(hg_plan *plan, int buffer, const void *host, size_t bytes, void *stream);
 int hg_plan_download(hg_plan *plan, int buffer, void *host, size_t bytes, void *stream);
 /* `steps` time steps, rotating the binding after each (runSerialStencil). */
 int hg_plan_run(hg_plan *plan, int64_t steps, void *stream);

@@ -77,7 +77,10 @@ std::vector<std::shared_ptr<Buffer>> runSerialStencil(ir::Operation &module,
   checkHg(hg_plan_create(&c.prog, device, &g.p), "hg_plan_create");
   for (int i = 0; i < c.prog.nfields; ++i) {
     auto &b = *fields[static_cast<std::size_t>(i)];
-    checkHg(hg_plan_upload(g.p, i, b.data.data(), b.data.size(), nullptr), "upload");
+    // with at least one step ahead, the output slot's store box is dead on arrival
+    checkHg((timesteps > 0 ? hg_plan_upload_live : hg_plan_upload)(g.p, i, b.data.data(),
+                                                                  b.data.size(), nullptr),
+            "upload");
   }
   checkHg(hg_plan_run(g.p, timesteps, nullptr), "hg_plan_run");
   for (int i = 0; i < c.prog.nfields; ++i) {

@@ -389,9 +389,12 @@ class Plan:
         check(lib().hg_plan_init_fields(self.h, _i64(origin) if origin is not None else None,
                                         stream))
 
-    def upload(self, b: int, arr: np.ndarray, stream=None):
+    def upload(self, b: int, arr: np.ndarray, stream=None, live: bool = False):
+        """live=True: skip the region the next step overwrites unread (hg_plan_upload_live);
+        run at least one step before reading the buffer back."""
         a = np.ascontiguousarray(arr, dtype=self.program.dtype)
-        check(lib().hg_plan_upload(self.h, b, a.ctypes.data_as(C.c_void_p), a.nbytes, stream))
+        fn = lib().hg_plan_upload_live if live else lib().hg_plan_upload
+        check(fn(self.h, b, a.ctypes.data_as(C.c_void_p), a.nbytes, stream))
 
     def download(self, b: int, out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
         lo, hi = self.program.field_bounds(b)
@@ -439,7 +442,7 @@ def run_serial_stencil(prog: Program, fields: List[Buffer], timesteps: int,
     plan = Plan(prog, device)
     try:
         for i, f in enumerate(fields):
-            plan.upload(i, f.data)
+            plan.upload(i, f.data, live=timesteps > 0)
         plan.run(timesteps)
         for i, f in enumerate(fields):
             plan.download(i, f.data)

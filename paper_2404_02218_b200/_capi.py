@@ -126,6 +126,7 @@ def lib() -> C.CDLL:
         "hg_plan_layout": (C.c_int, [V, C.c_int, P(HgLayout)]),
         "hg_plan_init_fields": (C.c_int, [V, P(I64), V]),
         "hg_plan_upload": (C.c_int, [V, C.c_int, V, SZ, V]),
+        "hg_plan_upload_live": (C.c_int, [V, C.c_int, V, SZ, V]),
         "hg_plan_download": (C.c_int, [V, C.c_int, V, SZ, V]),
         "hg_plan_run": (C.c_int, [V, I64, V]),
         "hg_plan_binding": (C.c_int, [V, P(I32), P(I64)]),

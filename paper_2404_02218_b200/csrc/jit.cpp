@@ -338,21 +338,23 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
       s << "      res" << k << ".v[" << j << "] = v" << p.result_op[k] << ";\n";
     s << "    }\n";
   }
-  // release plane m's stage only once every value read from it has been consumed: with two
-  // 16-byte loads per f64 window, releasing right after issuing the loads let the producer's
-  // next TMA land in the stage before the second load had read it (wrong f64 values when a
-  // dz = -1 window and a dy = -1 window coincide; tests/test_gpu_parity.py jit_f64 case)
-  s << "    __syncwarp();\n"
-       "    if (lane == 0) mb_arrive(&empty[sOld]);\n"
-       "    if (++sOld == NS) sOld = 0;\n";
   s << "    if (yok) {\n"
        "      const long long e = obase + (long long)m * P.plane;\n";
   for (int k = 0; k < p.nresults; ++k)
     s << "      if (xrem >= 4) st4(P.out[" << k << "] + e, res" << k << "); else "
       << "for (int j = 0; j < 4; ++j) if (j < xrem) P.out[" << k << "][e + j] = res" << k
       << ".v[j];\n";
-  s << "    }\n"
-       "  }\n"
+  s << "    }\n";
+  // release plane m's stage only once every value read from it has been consumed.  ptxas
+  // schedules LDS next to their first use, which may follow the arrive, and the SYNCS arrive
+  // does not wait for in-flight LDS: the producer's next TMA then lands in the stage before
+  // the load has read it (f64 windows, two LDS.128 each: flux3d per-apply tier, about 1 run
+  // in 10).  The arrive therefore follows the output stores, whose operands depend on every
+  // value the results use; a warp that stores nothing uses none of them.
+  s << "    __syncwarp();\n"
+       "    if (lane == 0) mb_arrive(&empty[sOld]);\n"
+       "    if (++sOld == NS) sOld = 0;\n";
+  s << "  }\n"
        "}\n";
   K.source = s.str();
   return HG_OK;

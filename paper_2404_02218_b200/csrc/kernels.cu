@@ -385,16 +385,6 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       else
         o.v[j] = add_(c, mul_(acc, P.scale));
     }
-    // Release a stage only after the values read from it are consumed: an arrive right after
-    // issuing the LDS let the producer's next TMA land in the stage before a load had read it
-    // (observed with f64 windows in the generated kernels).  Planes 0..R-1 fed only the queue
-    // and go with the first output plane.
-    release(sDone);
-    if (m == 0) {
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        release(i % NS);
-    }
     if (yok) {
       T *dst = outRow + int64_t(m) * P.plane;
       if (xrem >= 4) {
@@ -405,6 +395,18 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
           if (j < xrem)
             dst[j] = o.v[j];
       }
+    }
+    // Release a stage only once the values read from it are consumed.  ptxas may schedule an
+    // LDS after the arithmetic that precedes the arrive and complete it after the arrive (the
+    // SYNCS arrive does not wait for in-flight LDS), so the producer's next TMA could land in
+    // the stage first: the arrive follows the output stores, whose operands depend on every
+    // value loaded from the stage.  A warp with no store (rows past the domain) uses none of
+    // them.  Planes 0..R-1 fed only the queue and go with the first output plane.
+    release(sDone);
+    if (m == 0) {
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        release(i % NS);
     }
     return true;
   };
@@ -789,6 +791,64 @@ __global__ void initKernel(T *base, const DevLayout L, uint64_t seed, int64_t o0
   }
 }
 
+// ---- host <-> device field transfer (zero-copy over PCIe) ------------------------------------
+// Moves a field between the reference's packed host layout (row-major, halo included,
+// buffer.cpp:65-70) and the pitched device layout in ONE pass: the GPU reads (or writes) the
+// pinned, device-mapped host buffer directly, one warp per row, coalesced 128-byte requests,
+// UNROLL requests in flight per lane.  A pitched cudaMemcpy2DAsync upload runs at ~31 GB/s on
+// B200 against ~55 GB/s for a flat copy (tools/xfer_probe.py); this keeps the flat rate and
+// needs no staging buffer.  Rows or row parts inside the skip box [slo, shi) (raw indices) are
+// not moved: an upload skips the region the next step overwrites before reading it.
+template <typename T>
+__global__ void __launch_bounds__(256) hostXferKernel(T *dev, const DevLayout L, T *host, int up,
+                                                      int64_t slo0, int64_t shi0, int64_t slo1,
+                                                      int64_t shi1, int64_t slo2, int64_t shi2) {
+  constexpr int UNROLL = 8;
+  const int r = L.rank;
+  const int64_t W = L.shape[r - 1];
+  int64_t rows = 1;
+  for (int d = 0; d < r - 1; ++d)
+    rows *= L.shape[d];
+  const int64_t slo[3] = {slo0, slo1, slo2}, shi[3] = {shi0, shi1, shi2};
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += nw) {
+    // outer coordinates of the row; x-range of the skip box if the row lies inside it
+    bool inside = true;
+    int64_t rem = row;
+    for (int d = r - 2; d >= 0; --d) {
+      const int64_t c = rem % L.shape[d];
+      rem /= L.shape[d];
+      inside = inside && c >= slo[d] && c < shi[d];
+    }
+    const int64_t x0 = inside ? min(max(slo[r - 1], int64_t(0)), W) : W;
+    const int64_t x1 = inside ? min(max(shi[r - 1], x0), W) : W;
+    T *h = host + row * W;
+    T *d = dev + row * L.pitch + L.col0;
+    // the row minus [x0, x1): two runs [0, x0) and [x1, W)
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      const int64_t a = part ? x1 : 0, b = part ? W : x0;
+      for (int64_t x = a + lane; x < b; x += 32 * UNROLL) {
+        T v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (x + 32 * u < b)
+            v[u] = up ? h[x + 32 * u] : d[x + 32 * u];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (x + 32 * u < b) {
+            if (up)
+              d[x + 32 * u] = v[u];
+            else
+              h[x + 32 * u] = v[u];
+          }
+      }
+    }
+  }
+}
+
 // ---- box copies -----------------------------------------------------------------------------
 template <typename T>
 __global__ void packKernel(T *base, const DevLayout L, int64_t a0, int64_t a1, int64_t a2,
@@ -1116,6 +1176,27 @@ int launchCopyBox(const void *src, const DevLayout &sl, void *dst, const DevLayo
                                                   static_cast<double *>(dst), dl, l[0], l[1],
                                                   l[2], e[0], e[1], e[2]);
   return cudaErr(cudaGetLastError(), "copy kernel launch");
+}
+
+int launchHostXfer(void *dev, const DevLayout &lay, void *host_dev, int up, const int64_t *skip_lo,
+                   const int64_t *skip_hi, cudaStream_t st) {
+  int64_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0}; // empty box: move everything
+  if (skip_lo && skip_hi)
+    for (int d = 0; d < lay.rank; ++d) {
+      lo[d] = skip_lo[d];
+      hi[d] = skip_hi[d];
+    }
+  // enough warps to keep ~10 MB of PCIe requests in flight; grid in multiples of the SMs
+  const unsigned blocks = 148 * 8;
+  if (lay.es == 4)
+    hostXferKernel<float><<<blocks, 256, 0, st>>>(static_cast<float *>(dev), lay,
+                                                  static_cast<float *>(host_dev), up, lo[0], hi[0],
+                                                  lo[1], hi[1], lo[2], hi[2]);
+  else
+    hostXferKernel<double><<<blocks, 256, 0, st>>>(static_cast<double *>(dev), lay,
+                                                   static_cast<double *>(host_dev), up, lo[0],
+                                                   hi[0], lo[1], hi[1], lo[2], hi[2]);
+  return cudaErr(cudaGetLastError(), "host transfer kernel launch");
 }
 
 int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,

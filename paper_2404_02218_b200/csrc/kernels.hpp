@@ -97,6 +97,11 @@ int launchInit(void *base, const DevLayout &lay, int field, const int64_t *origi
 // stencil.store between layouts: dst[p] = src[p] for logical points p in [lb, ub)
 int launchCopyBox(const void *src, const DevLayout &sl, void *dst, const DevLayout &dl,
                   const int64_t *lb, const int64_t *ub, cudaStream_t st);
+// host <-> device copy of a whole field (up = 1: host -> device) through the device-mapped
+// pointer of a pinned host buffer in the reference's packed layout; raw box [skip_lo, skip_hi)
+// is not moved (both NULL: move everything)
+int launchHostXfer(void *dev, const DevLayout &lay, void *host_dev, int up, const int64_t *skip_lo,
+                   const int64_t *skip_hi, cudaStream_t st);
 // box copy between a layout box and a packed array (dir 0 = pack, 1 = unpack)
 int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,
                      void *packed, int unpack, cudaStream_t st);

@@ -671,7 +671,20 @@ int hg_plan_init_fields(hg_plan *p, const int64_t *origin, void *stream) {
   return HG_OK;
 }
 
-static int copy2d(hg_plan *p, int b, void *host, size_t bytes, void *stream, bool up) {
+// Device-accessible address of a pinned host buffer (cudaHostAlloc / cudaHostRegister, mapped
+// under unified addressing), or null for pageable memory.
+static void *mappedHost(void *host) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+    cudaGetLastError(); // pageable memory on older runtimes reports an error; not sticky
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+// skip_lo/hi: raw box of buffer b not to move (uploads only; null = move everything)
+static int copyField(hg_plan *p, int b, void *host, size_t bytes, void *stream, bool up,
+                     const int64_t *skip_lo, const int64_t *skip_hi) {
   if (!p || b < 0 || b >= static_cast<int>(p->lay.size()))
     return setError(HG_EINVAL, "bad plan/buffer");
   const Layout &L = p->lay[static_cast<size_t>(b)];
@@ -680,27 +693,78 @@ static int copy2d(hg_plan *p, int b, void *host, size_t bytes, void *stream, boo
   int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice");
   if (st)
     return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (void *hd = mappedHost(host)) {
+    // pinned host memory: one zero-copy pass at the flat PCIe rate (kernels.cu hostXferKernel)
+    st = launchHostXfer(p->dptr[static_cast<size_t>(b)], devLayout(L), hd, up ? 1 : 0, skip_lo,
+                        skip_hi, s);
+    ++p->launches;
+    if (!st && !up)
+      st = cudaCheck(cudaStreamSynchronize(s), "download");
+    return st;
+  }
+  // pageable memory: the copy engines, one pitched copy of the whole field
   const size_t w = static_cast<size_t>(L.shape[L.rank - 1]) * L.es;
   char *dev = static_cast<char *>(p->dptr[static_cast<size_t>(b)]) + L.col0 * L.es;
   const size_t dp = static_cast<size_t>(L.pitch) * L.es;
   cudaError_t e =
       up ? cudaMemcpy2DAsync(dev, dp, host, w, w, static_cast<size_t>(L.rows),
-                             cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream))
+                             cudaMemcpyHostToDevice, s)
          : cudaMemcpy2DAsync(host, w, dev, dp, w, static_cast<size_t>(L.rows),
-                             cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
+                             cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && !up)
-    e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    e = cudaStreamSynchronize(s);
   return cudaCheck(e, up ? "upload" : "download");
 }
 
 int hg_plan_upload(hg_plan *p, int b, const void *host, size_t bytes, void *stream) {
   if (p && b >= 0 && b < static_cast<int>(p->shadowOk.size()))
     p->shadowOk[static_cast<size_t>(b)] = 0;
-  return copy2d(p, b, const_cast<void *>(host), bytes, stream, true);
+  return copyField(p, b, const_cast<void *>(host), bytes, stream, true, nullptr, nullptr);
+}
+
+int hg_plan_upload_live(hg_plan *p, int b, const void *host, size_t bytes, void *stream) {
+  if (!p || b < 0 || b >= static_cast<int>(p->lay.size()))
+    return setError(HG_EINVAL, "bad plan/buffer");
+  if (b < static_cast<int>(p->shadowOk.size()))
+    p->shadowOk[static_cast<size_t>(b)] = 0;
+  // The slot buffer b is bound to now; the next step's stores into it and its loads.
+  const hg_program &g = p->prog;
+  int slot = -1;
+  for (size_t i = 0; i < p->bind.size(); ++i)
+    if (p->bind[i] == b)
+      slot = static_cast<int>(i);
+  bool loaded = false;
+  for (int o = 0; o < g.noperands; ++o)
+    loaded = loaded || g.operand_field[o] == slot;
+  const hg_bounds *box = nullptr;
+  int nbox = 0;
+  if (g.napplies > 0) {
+    for (int k = 0; k < g.nstores; ++k)
+      if (g.mstore_field[k] == slot) {
+        box = &g.mstore[k];
+        ++nbox;
+      }
+  } else {
+    for (int k = 0; k < g.nresults; ++k)
+      if (g.store_field[k] == slot) {
+        box = &g.store[k];
+        ++nbox;
+      }
+  }
+  if (slot < 0 || loaded || nbox != 1) // nothing the next step overwrites unread
+    return copyField(p, b, const_cast<void *>(host), bytes, stream, true, nullptr, nullptr);
+  const Layout &L = p->lay[static_cast<size_t>(b)];
+  int64_t lo[3], hi[3];
+  for (int d = 0; d < L.rank; ++d) {
+    lo[d] = box->lb[d] - L.lb[d];
+    hi[d] = box->ub[d] - L.lb[d];
+  }
+  return copyField(p, b, const_cast<void *>(host), bytes, stream, true, lo, hi);
 }
 
 int hg_plan_download(hg_plan *p, int b, void *host, size_t bytes, void *stream) {
-  return copy2d(p, b, host, bytes, stream, false);
+  return copyField(p, b, host, bytes, stream, false, nullptr, nullptr);
 }
 
 } // extern "C"

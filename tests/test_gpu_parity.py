@@ -361,3 +361,88 @@ def test_multi_apply_flux3d_medium(port, monkeypatch, family, prefix):
     assert perm == perm_o
     for g, o in zip(fin, [arrays[p] for p in perm_o]):
         assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
+_SHALLOW_RING = r"""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.environ["REPO"]); sys.path.insert(0, os.path.join(os.environ["REPO"], "oracle"))
+import paper_2404_02218_b200 as hg
+from oracle import Port
+from paper_2404_02218_b200.programs.flux3d import xir
+from paper_2404_02218_b200.programs.pw_advection import xir as pw_xir
+port = Port()
+cases = [(hg.Program.parse(xir(12, 10, 21, "f64"))[0], 3),
+         (hg.Program.parse(xir(7, 9, 8, "f64"))[0], 3),
+         (hg.Program.parse(pw_xir(9, 10, 11, "f64"))[0], 2)]
+bad = 0
+for prog, T in cases:
+    arrays = port.initial_fields(prog)
+    want = [arrays[p] for p in port.run(prog, arrays, T)]
+    for rep in range(8):
+        plan = hg.Plan(prog); plan.init_fields(); plan.run(T)
+        perm, _ = plan.binding()
+        got = [plan.download(p) for p in perm]
+        plan.close()
+        bad += sum(int(not np.array_equal(g.view(np.uint64), w.view(np.uint64)))
+                   for g, w in zip(got, want))
+print("bad", bad)
+sys.exit(1 if bad else 0)
+"""
+
+
+@pytest.mark.parametrize("fuse", ["per-apply", "fused"])
+def test_shallow_tma_ring_reuse_bitwise(fuse):
+    # Stage-reuse hazard of the TMA ring: with a ring only one plane deeper than the stencil
+    # window (HG_JIT_DEPTH=1) every stage is refilled while neighbouring warps still stream.
+    # An arrive that did not follow the consumption of the loaded values let the refill land
+    # before an f64 window's second LDS.128 had read it (failed every run before the fix).
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, REPO=repo, HG_JIT_DEPTH="1")
+    if fuse == "per-apply":
+        env["HG_NO_FUSE_APPLIES"] = "1"
+    r = subprocess.run([sys.executable, "-c", _SHALLOW_RING], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("spec,T", [(("heat", 3, 67, 4), 3), (("wave", 3, 45, 8), 4),
+                                    (("heat", 2, 301, 2), 5), (("heat", 3, 40, 2), 1)])
+def test_host_transfers_and_live_upload(port, pinned, spec, T):
+    # uploads/downloads from pinned host memory (zero-copy kernel) and pageable memory (copy
+    # engines); the live upload leaves the output slot's store box unmoved -- garbage there
+    # must not matter, since step 1 overwrites it before anything reads it
+    import torch
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    arrays = port.initial_fields(prog)
+    plan = hg.Plan(prog)
+    try:
+        # poison every buffer first, so a skipped region that mattered would show
+        for i in range(prog.nfields):
+            plan.upload(i, np.full_like(arrays[i], np.float32(1e30)))
+        hosts = []
+        for i, a in enumerate(arrays):
+            h = torch.from_numpy(a.copy()).pin_memory().numpy() if pinned else a.copy()
+            hosts.append(h)
+            plan.upload(i, h, live=True)
+        # a full upload of buffer 0 round-trips exactly
+        back = plan.download(0)
+        assert np.array_equal(back.view(np.uint32), arrays[0].view(np.uint32))
+        plan.run(T)
+        perm, _ = plan.binding()
+        outs = []
+        for p in perm:
+            o = np.empty_like(arrays[p])
+            if pinned:
+                o = torch.from_numpy(o).pin_memory().numpy()
+            outs.append(plan.download(p, o))
+    finally:
+        plan.close()
+    perm_o = port.run(prog, arrays, T)
+    assert perm == perm_o
+    for g, p in zip(outs, perm_o):
+        assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
