@@ -168,6 +168,28 @@ def cpu_baseline(workload="heat3d_weak"):
             "seconds": secs}
 
 
+def bind_host_to_gpu_numa(device: int):
+    """Run this rank's host threads (and first-touch its pinned buffers) on the CPUs of the
+    GPU's own NUMA node, so concurrent ranks' PCIe traffic does not cross the socket link.
+    Best effort: returns the cpulist used, or None."""
+    import torch
+    try:
+        p = torch.cuda.get_device_properties(device)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return spec
+    except Exception:
+        return None
+    return None
+
+
 def dead_on_arrival_bytes(prog, es):
     """Bytes hg_plan_upload_live skips with the initial binding: the store box of every slot
     the step stores into (one store) without loading it (mirrors plan.cpp)."""
@@ -246,6 +268,7 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    numa_cpus = bind_host_to_gpu_numa(local_rank)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
@@ -400,7 +423,7 @@ def run_ours(args):
                        f"(zero-copy kernel; the output slot's core, overwritten unread by "
                        f"step 1, is not moved), {T} time steps, download the final binding "
                        f"(per rank)",
-               "calls": n_calls}
+               "calls": n_calls, "host_cpus": numa_cpus}
 
     if rank == 0:
         clocks = clk.summary()

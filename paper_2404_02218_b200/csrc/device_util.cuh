@@ -24,6 +24,45 @@ __device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
 
+// ---- packed f32x2 arithmetic (FADD2/FMUL2: two independent IEEE RN f32 ops per issue) -------
+// Each lane of add/mul.rn.f32x2 is the scalar RN op, so packing two points' identical op
+// sequences is bit-exact -- provided nothing is contracted.  ptxas fuses mul.rn.f32x2 ->
+// add.rn.f32x2 into FFMA2 even under -fmad=false (profiles/r1_sweeps.md); pfence() makes a
+// product opaque (OR of a run-time zero into its low word, one ALU op) so every product is
+// rounded before its add, exactly as the reference's -ffp-contract=off code does.
+using f2 = unsigned long long;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(f2 v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 pfence(f2 v, uint32_t zero) {
+  uint32_t lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+  lo |= zero;
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
 template <typename T> __host__ __device__ inline T fromBits(uint64_t b);
 template <> __host__ __device__ inline float fromBits<float>(uint64_t b) {
   uint32_t u = static_cast<uint32_t>(b);

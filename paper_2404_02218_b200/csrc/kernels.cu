@@ -103,6 +103,14 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
   static constexpr int TXT = 32, TYT = 1;
 };
 
+// f32 star arithmetic on packed f32x2 pairs: bit-exact, but measured 4-8% slower than the
+// scalar form (pair-forming moves, fences, weight registers; profiles/r1_sweeps.md), so the
+// product builds the scalar form; HG_PACK=1 builds the packed one for A/B
+#ifndef HG_PACK
+#define HG_PACK 0
+#endif
+template <typename T> constexpr bool kPackF32 = HG_PACK && std::is_same<T, float>::value;
+
 template <typename T> struct StarParams {
   int64_t plane;   // elements between consecutive dim-0 planes
   int64_t pitch;   // elements between rows of the last dim
@@ -131,6 +139,10 @@ template <typename T> struct StarParams {
   int boundary_last;
   T *out;
   T w0, wz[3], wy[3], wx[3], scale, two;
+  // f32 packed path: the same weights as {w, w} pairs (uniform registers) and a zero that
+  // only the host knows is zero (pfence)
+  unsigned long long pw0, pwz[3], pwy[3], pwx[3], pscale, ptwo;
+  uint32_t zero;
 };
 
 template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
@@ -356,6 +368,51 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
 
     constexpr int cz = (U + R) % Q;
     V4<T> o;
+    if constexpr (kPackF32<T>) {
+      // points (j, j+1) as one f32x2 lane pair: the same op sequence as the scalar branch
+      // below, every product fenced (see pfence)
+      const uint32_t z0 = P.zero;
+      auto win = [&](int i) -> T { // window [L | centre | Rr]
+        return i < 4 ? L.v[i & 3] : (i < 8 ? q[cz][i & 3] : Rr.v[i & 3]);
+      };
+#pragma unroll
+      for (int j = 0; j < 4; j += 2) {
+        const f2 c = pk2(q[cz][j], q[cz][j + 1]);
+        f2 acc = pfence(mul2(c, P.pw0), z0);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int k = Taps<NT>::k(t);
+          const int zp = (U + R + k) % Q, zm = (U + R - k + Q) % Q;
+          acc = add2(acc, pfence(mul2(add2(pk2(q[zp][j], q[zp][j + 1]),
+                                           pk2(q[zm][j], q[zm][j + 1])),
+                                      P.pwz[t]),
+                                 z0));
+        }
+        if constexpr (RANK == 3) {
+#pragma unroll
+          for (int t = 0; t < NT; ++t)
+            acc = add2(acc, pfence(mul2(add2(pk2(yp[t].v[j], yp[t].v[j + 1]),
+                                             pk2(ym[t].v[j], ym[t].v[j + 1])),
+                                        P.pwy[t]),
+                                   z0));
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int k = Taps<NT>::k(t);
+          acc = add2(acc, pfence(mul2(add2(pk2(win(4 + j + k), win(5 + j + k)),
+                                           pk2(win(4 + j - k), win(5 + j - k))),
+                                      P.pwx[t]),
+                                 z0));
+        }
+        f2 r;
+        if constexpr (C::WAVE)
+          r = add2(sub2(pfence(mul2(c, P.ptwo), z0), pk2(pv.v[j], pv.v[j + 1])),
+                   pfence(mul2(acc, P.pscale), z0));
+        else
+          r = add2(c, pfence(mul2(acc, P.pscale), z0));
+        upk2(r, o.v[j], o.v[j + 1]);
+      }
+    } else {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const T c = q[cz][j];
@@ -384,6 +441,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         o.v[j] = add_(sub_(mul_(c, P.two), pv.v[j]), mul_(acc, P.scale));
       else
         o.v[j] = add_(c, mul_(acc, P.scale));
+    }
     }
     if (yok) {
       T *dst = outRow + int64_t(m) * P.plane;
@@ -594,6 +652,18 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   }
   P.scale = fromBits<T>(s.scale);
   P.two = fromBits<T>(s.two);
+  {
+    auto pair = [](uint64_t b) { return (b & 0xffffffffull) | ((b & 0xffffffffull) << 32); };
+    P.pw0 = pair(s.w0);
+    for (int t = 0; t < 3; ++t) {
+      P.pwz[t] = pair(s.w[0][t]);
+      P.pwy[t] = pair(s.w[RANK == 3 ? 1 : 0][t]);
+      P.pwx[t] = pair(s.w[RANK - 1][t]);
+    }
+    P.pscale = pair(s.scale);
+    P.ptwo = pair(s.two);
+    P.zero = 0;
+  }
   P.cy = 1;
   if (RANK == 3) {
     P.cy = HG_CLUSTER_Y;
@@ -799,51 +869,95 @@ __global__ void initKernel(T *base, const DevLayout L, uint64_t seed, int64_t o0
 // B200 against ~55 GB/s for a flat copy (tools/xfer_probe.py); this keeps the flat rate and
 // needs no staging buffer.  Rows or row parts inside the skip box [slo, shi) (raw indices) are
 // not moved: an upload skips the region the next step overwrites before reading it.
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; };
+template <> struct Vec16<double> { using type = double2; };
+
 template <typename T>
 __global__ void __launch_bounds__(256) hostXferKernel(T *dev, const DevLayout L, T *host, int up,
                                                       int64_t slo0, int64_t shi0, int64_t slo1,
                                                       int64_t shi1, int64_t slo2, int64_t shi2) {
-  constexpr int UNROLL = 8;
+  // The host array is contiguous (the pitch is a device-side artefact), so threads walk it in
+  // 16-byte chunks: one 16-byte PCIe access per thread, 512 bytes per warp instruction, UNROLL
+  // in flight per thread.  Each element of a chunk is then placed into its pitched row.
+  using V = typename Vec16<T>::type;
+  constexpr int NV = 16 / sizeof(T), UNROLL = 4;
   const int r = L.rank;
   const int64_t W = L.shape[r - 1];
-  int64_t rows = 1;
-  for (int d = 0; d < r - 1; ++d)
-    rows *= L.shape[d];
+  int64_t total = 1;
+  for (int d = 0; d < r; ++d)
+    total *= L.shape[d];
   const int64_t slo[3] = {slo0, slo1, slo2}, shi[3] = {shi0, shi1, shi2};
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t row = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
-       row += nw) {
-    // outer coordinates of the row; x-range of the skip box if the row lies inside it
-    bool inside = true;
+  const bool anySkip = slo[r - 1] < shi[r - 1];
+  // row -> (inside the skip box in the outer dims, device row offset)
+  auto rowInfo = [&](int64_t row, bool &inside) {
+    inside = anySkip;
     int64_t rem = row;
     for (int d = r - 2; d >= 0; --d) {
       const int64_t c = rem % L.shape[d];
       rem /= L.shape[d];
       inside = inside && c >= slo[d] && c < shi[d];
     }
-    const int64_t x0 = inside ? min(max(slo[r - 1], int64_t(0)), W) : W;
-    const int64_t x1 = inside ? min(max(shi[r - 1], x0), W) : W;
-    T *h = host + row * W;
-    T *d = dev + row * L.pitch + L.col0;
-    // the row minus [x0, x1): two runs [0, x0) and [x1, W)
-#pragma unroll 1
-    for (int part = 0; part < 2; ++part) {
-      const int64_t a = part ? x1 : 0, b = part ? W : x0;
-      for (int64_t x = a + lane; x < b; x += 32 * UNROLL) {
-        T v[UNROLL];
+    return row * L.pitch + L.col0;
+  };
+  const int64_t nchunks = (total + NV - 1) / NV;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t c0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c0 < nchunks;
+       c0 += stride * UNROLL) {
+    V v[UNROLL];
+    int64_t row[UNROLL], x[UNROLL], drow[UNROLL];
+    bool ins[UNROLL], need[UNROLL];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-          if (x + 32 * u < b)
-            v[u] = up ? h[x + 32 * u] : d[x + 32 * u];
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t c = c0 + stride * u;
+      need[u] = c < nchunks;
+      if (!need[u])
+        continue;
+      const int64_t e = c * NV;
+      row[u] = e / W;
+      x[u] = e - row[u] * W;
+      drow[u] = rowInfo(row[u], ins[u]);
+      // a chunk entirely inside the skip box (same row, x range inside) is not moved
+      if (ins[u] && x[u] >= slo[r - 1] && x[u] + NV <= shi[r - 1] && x[u] + NV <= W)
+        need[u] = false;
+      if (need[u] && up) {
+        if (e + NV <= total)
+          v[u] = reinterpret_cast<const V *>(host)[c];
+        else
+          for (int j = 0; j < NV; ++j)
+            reinterpret_cast<T *>(&v[u])[j] = e + j < total ? host[e + j] : T(0);
+      }
+    }
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-          if (x + 32 * u < b) {
-            if (up)
-              d[x + 32 * u] = v[u];
-            else
-              h[x + 32 * u] = v[u];
-          }
+    for (int u = 0; u < UNROLL; ++u) {
+      if (!need[u])
+        continue;
+      const int64_t e = (c0 + stride * u) * NV;
+      int64_t rw = row[u], xx = x[u], dr = drow[u];
+      bool in = ins[u];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        if (e + j >= total)
+          break;
+        if (xx == W) { // the chunk runs into the next row
+          ++rw;
+          xx = 0;
+          dr = rowInfo(rw, in);
+        }
+        if (up) {
+          if (!(in && xx >= slo[r - 1] && xx < shi[r - 1]))
+            dev[dr + xx] = reinterpret_cast<const T *>(&v[u])[j];
+        } else {
+          reinterpret_cast<T *>(&v[u])[j] = dev[dr + xx];
+        }
+        ++xx;
+      }
+      if (!up) {
+        if (e + NV <= total)
+          reinterpret_cast<V *>(host)[c0 + stride * u] = v[u];
+        else
+          for (int j = 0; j < NV && e + j < total; ++j)
+            host[e + j] = reinterpret_cast<const T *>(&v[u])[j];
       }
     }
   }

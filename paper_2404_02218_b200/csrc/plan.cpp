@@ -694,7 +694,11 @@ static int copyField(hg_plan *p, int b, void *host, size_t bytes, void *stream, 
   if (st)
     return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (void *hd = mappedHost(host)) {
+  static const char *force = std::getenv("HG_XFER"); // "ce": copy engines only (A/B)
+  // downloads: the copy engines' pitched copy already runs at the flat rate (52 GB/s vs 51 for
+  // the kernel, tools/xfer_probe.py); uploads: the zero-copy kernel (51 vs 31 GB/s)
+  void *hd = !up || (force && force[0] == 'c') ? nullptr : mappedHost(host);
+  if (hd && reinterpret_cast<uintptr_t>(hd) % 16 == 0) {
     // pinned host memory: one zero-copy pass at the flat PCIe rate (kernels.cu hostXferKernel)
     st = launchHostXfer(p->dptr[static_cast<size_t>(b)], devLayout(L), hd, up ? 1 : 0, skip_lo,
                         skip_hi, s);
