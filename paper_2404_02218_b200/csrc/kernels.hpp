@@ -76,6 +76,22 @@ int launchTb(const TbLaunch &L, cudaStream_t st, int *blocks_out);
 int makeBoxTensorMap(int dtype, const DevLayout &lay, void *base, const uint32_t box[3],
                      CUtensorMap *out);
 
+// ---- whole-run 2D heat with shared-memory-resident fields (resident.cu) -------------------
+struct ResLaunch {
+  const StarSpec *spec;
+  int dtype;
+  DevLayout lay;             // shared by both buffers
+  int64_t start[2], ext[2];  // store box, raw indices
+  void *in, *out;            // buffers bound to the star's cur operand and its store slot
+  void *xbuf;                // exchange rows (residentSupported: bytes)
+  unsigned long long *flags; // one word per CTA, monotonically increasing epochs
+  unsigned long long epoch;  // larger than every flag value of earlier launches
+  unsigned tag0;             // f32: block tags tag0+1 .. tag0+blocks unused by earlier launches
+  int64_t steps;
+};
+bool residentSupported(const ResLaunch &L, size_t *xbufBytes, int *ctas);
+int launchResident(const ResLaunch &L, cudaStream_t st);
+
 // ---- generic bytecode kernel ------------------------------------------------------------
 struct GenericLaunch {
   int dtype, rank;

@@ -613,6 +613,10 @@ int hg_plan_destroy(hg_plan *p) {
       cudaFree(d);
   for (void *d : p->tmpPtr)
     cudaFree(d);
+  if (p->resXbuf)
+    cudaFree(p->resXbuf);
+  if (p->resFlags)
+    cudaFree(p->resFlags);
   for (auto &m : p->multi)
     cudaFree(m.ops);
   if (p->gopsDev)
@@ -630,6 +634,8 @@ int hg_plan_kernel_name(const hg_plan *p, char *name, size_t cap) {
                                             (p->prog.dtype == HG_F32 ? "f32" : "f64"));
   if (tbEligible(*p))
     n += "+tb2"; // runs of >= 2 steps go through two-step passes (tb.cu)
+  if (residentEligible(*p))
+    n += "+resident"; // runs go through one shared-memory-resident launch (resident.cu)
   if (name && cap)
     std::snprintf(name, cap, "%s", n.c_str());
   return HG_OK;
@@ -791,6 +797,92 @@ bool tbEligible(const hg_plan &p) {
 
 namespace {
 
+ResLaunch residentLaunchOf(const hg_plan &p) {
+  const hg_program &g = p.prog;
+  const StarSpec &sp = p.an.star;
+  ResLaunch L{};
+  L.spec = &sp;
+  L.dtype = g.dtype;
+  const int bIn = p.bind[static_cast<size_t>(g.operand_field[sp.cur_operand])];
+  const int bOut = p.bind[static_cast<size_t>(g.store_field[0])];
+  const Layout &lay = p.lay[static_cast<size_t>(bOut)];
+  L.lay = devLayout(lay);
+  for (int d = 0; d < 2; ++d) {
+    L.start[d] = g.store[0].lb[d] - lay.lb[d];
+    L.ext[d] = g.store[0].ub[d] - g.store[0].lb[d];
+  }
+  L.in = p.dptr[static_cast<size_t>(bIn)];
+  L.out = p.dptr[static_cast<size_t>(bOut)];
+  return L;
+}
+
+} // namespace
+
+// Small 2D heat plans (both fields fit in the SMs' shared memory) run whole calls in one
+// resident launch; HG_NO_RESIDENT=1 keeps the per-step star kernel (A/B, tests).
+bool residentEligible(const hg_plan &p) {
+  if (std::getenv("HG_NO_RESIDENT") || p.tbOff || p.an.family != Family::Star || p.prog.rank != 2 ||
+      p.an.star.kind != kHeat || p.prog.nresults != 1 || p.bind.size() != 2)
+    return false;
+  const ResLaunch L = residentLaunchOf(p);
+  return L.in != L.out && residentSupported(L, nullptr, nullptr);
+}
+
+namespace {
+
+int runResident(hg_plan &p, int64_t steps, cudaStream_t s) {
+  ResLaunch L = residentLaunchOf(p);
+  size_t xb = 0;
+  int ctas = 0;
+  if (!residentSupported(L, &xb, &ctas))
+    return setError(HG_EUNSUPPORTED, "resident 2D kernel: plan does not fit");
+  if (xb > p.resXbufBytes) {
+    if (p.resXbuf)
+      cudaFree(p.resXbuf);
+    p.resXbuf = nullptr;
+    int st = cudaCheck(cudaMalloc(&p.resXbuf, xb), "cudaMalloc(resident exchange)");
+    // tagged words: a stale word (e.g. an earlier plan's allocation) must not carry a live tag
+    if (!st)
+      st = cudaCheck(cudaMemsetAsync(p.resXbuf, 0, xb, s), "cudaMemset(resident exchange)");
+    if (st)
+      return st;
+    p.resTag = 0;
+    p.resXbufBytes = xb;
+  }
+  if (ctas > p.resCtas) {
+    if (p.resFlags)
+      cudaFree(p.resFlags);
+    p.resFlags = nullptr;
+    int st = cudaCheck(cudaMalloc(&p.resFlags, sizeof(unsigned long long) * ctas),
+                       "cudaMalloc(resident flags)");
+    if (!st)
+      st = cudaCheck(cudaMemsetAsync(p.resFlags, 0, sizeof(unsigned long long) * ctas, s),
+                     "cudaMemset(resident flags)");
+    if (st)
+      return st;
+    p.resCtas = ctas;
+    p.resLaunches = 0;
+  }
+  L.xbuf = p.resXbuf;
+  L.flags = p.resFlags;
+  L.epoch = (++p.resLaunches) << 32; // above every epoch an earlier launch published
+  L.tag0 = p.resTag;                  // tags tag0+1 .. tag0+blocks (blocks <= steps)
+  p.resTag += static_cast<unsigned>(steps) + 1u;
+  L.steps = steps;
+  int st = launchResident(L, s);
+  if (st)
+    return st;
+  ++p.launches;
+  for (int64_t t = 0; t < steps; ++t) { // the rotation the steps performed
+    std::vector<int> nxt(p.bind.size());
+    for (size_t i = 0; i < p.bind.size(); ++i)
+      nxt[i] = p.bind[static_cast<size_t>(p.an.src[i])];
+    p.bind.swap(nxt);
+  }
+  p.stepsDone += steps;
+  return HG_OK;
+}
+
 // Shadow of buffer b: same layout, same halo ring (a full copy once; the ring is never
 // written by a step, and the plan's own writers invalidate it).
 int ensureShadow(hg_plan &p, int b, cudaStream_t s) {
@@ -894,6 +986,8 @@ int hg_plan_run(hg_plan *p, int64_t steps, void *stream) {
   if (st)
     return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (steps >= 1 && steps < (int64_t(1) << 31) && residentEligible(*p))
+    return runResident(*p, steps, s);
   if (steps >= 2 && tbEligible(*p)) {
     // pairs of steps; an odd step count ends with one ordinary step, which then also writes
     // the t+1 buffer, so only an even count needs the last pair to store its t+1 core

@@ -61,6 +61,13 @@ struct hg_plan {
   bool tbOff = false;                 // set once a dmp exported the buffers
   std::string namePrefix;             // "multiNx_fused_" when the applies were fused
   int64_t tbPasses = 0;
+  // whole-run resident 2D kernel (resident.cu): exchange rows + per-CTA epoch flags
+  void *resXbuf = nullptr;
+  size_t resXbufBytes = 0;
+  unsigned long long *resFlags = nullptr;
+  int resCtas = 0;
+  unsigned long long resLaunches = 0;
+  unsigned resTag = 0;
 };
 
 namespace hg {
@@ -69,6 +76,8 @@ int cudaCheck(cudaError_t e, const char *what);
 int planStep(hg_plan &p, cudaStream_t st);
 // Whether hg_plan_run advances this plan by two-step passes (tb.cu).
 bool tbEligible(const hg_plan &p);
+// Whether hg_plan_run runs this plan's steps in one resident launch (resident.cu).
+bool residentEligible(const hg_plan &p);
 } // namespace hg
 
 #endif

@@ -1,0 +1,432 @@
+// resident.cu -- whole-run 2D heat stencil with the fields resident in shared memory.
+//
+// BASELINE config 1 (heat 2D SDO2, 1024^2 f32, 100 steps) moves 8 MB per step: the per-step
+// star kernel is launch/latency-bound there (3.6 us per step with CUDA-graph replay, most of
+// it launch and pipeline fill).  On B200 the two ping-pong fields fit in the 148 SMs' shared
+// memory (2 x 4.2 MB against 148 x 227 KB), so one persistent launch runs ALL T steps:
+//
+//   * CTA c owns a band of store rows [r0, r1) and keeps, for both buffers, the rows
+//     [r0 - E, r1 + E) (E = K*R, K = 2 steps per exchange) at full allocated width in shared
+//     memory -- each tile with its own buffer's halo ring (the reference never writes outside
+//     the store box, interpreter.cpp:683-712, so those cells stay the buffer's initial values).
+//   * Temporal blocking: K steps run back to back on the tile, the computed rows shrinking by
+//     R per step ([r0 - (K-1-s)R, r1 + (K-1-s)R) at sub-step s); only then do neighbours
+//     exchange the E boundary rows of the current time level through L2 (double-buffered
+//     exchange slots; f32 values travel in 64-bit words tagged with the block number, so the
+//     data is its own flag; f64 uses a per-CTA epoch flag with gpu-scope release/acquire).
+//     The redundant rows are recomputed with the same op sequence: bit-identical values.
+//   * At the end, each CTA writes the store rows of both tiles back to HBM.
+//
+// Bit-exactness: the per-point DAG is starKernel's (lap = c*w0, then dim 0 taps ascending,
+// then dim 1; u + lap*scale), one IEEE RN op at a time (kernels.cpp:110-135).
+// Co-residency of the spinning CTAs is guaranteed by a cooperative launch (<= 1 CTA per SM).
+#include "device_util.cuh"
+#include "kernels.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+namespace hg {
+namespace {
+
+int cudaErrRes(cudaError_t e, const char *what) {
+  if (e == cudaSuccess)
+    return HG_OK;
+  return setError(HG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kResThreads = 512;
+
+template <typename T> struct ResParams {
+  T *buf[2];                  // tile 0 = buffer bound to the in slot, tile 1 = the out slot
+  T *xbuf;                    // exchange rows [2 parities][G][2 sides][E][nx]
+  unsigned long long *flags;  // per CTA: last exchange published (cumulative epochs)
+  unsigned long long epoch;   // flags value before this launch
+  unsigned tag0;              // f32 tagged exchange: block tags of this launch are tag0+1..
+  int64_t pitch, col0;        // device layout
+  int H, W;                   // allocated rows / columns (raw)
+  int s0r, s0c;               // raw start row / column of the store box
+  int ny, nx;                 // store box extents
+  int steps, K, E;            // time steps, steps per exchange, exchanged rows (K*R)
+  int maxRows;                // largest band
+  int SP, PL;                 // shared row pitch (elements) and left pad
+  T w0, wz[3], wx[3], scale;
+};
+
+template <typename T>
+__device__ __forceinline__ void bandOf(int ny, int G, int c, int &r0, int &r1) {
+  const int base = ny / G, extra = ny % G;
+  r0 = c * base + min(c, extra);
+  r1 = r0 + base + (c < extra ? 1 : 0);
+}
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(kResThreads, 1) residentKernel(const ResParams<T> P) {
+  constexpr int R = Taps<NT>::R;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+  int r0, r1;
+  bandOf<T>(P.ny, G, c, r0, r1);
+  const int E = P.E;
+  const int tileRows = P.maxRows + 2 * E;
+  T *const tile0 = reinterpret_cast<T *>(smraw);
+  T *const tile1 = tile0 + size_t(tileRows) * P.SP;
+  auto tile = [&](int b) { return b ? tile1 : tile0; }; // no local-memory array
+  // tile row i <-> raw row lo + i
+  const int lo = P.s0r + r0 - E;
+  const int nrows = (r1 - r0) + 2 * E;
+
+  // ---- load both buffers' rows (full allocated width: the halo ring comes along) ----
+  for (int b = 0; b < 2; ++b) {
+    const T *g = b ? P.buf[1] : P.buf[0];
+    T *t = tile(b);
+    for (int64_t k = tid; k < int64_t(nrows) * P.W; k += kResThreads) {
+      const int i = int(k / P.W), x = int(k % P.W);
+      const int raw = lo + i;
+      if (raw >= 0 && raw < P.H)
+        t[size_t(i) * P.SP + P.PL + x] = g[int64_t(raw) * P.pitch + P.col0 + x];
+    }
+  }
+  __syncthreads();
+
+  const int ngx = (P.nx + 3) / 4;
+  const int gy0 = tid / ngx, gx0 = tid % ngx, dgy = kResThreads / ngx, dgx = kResThreads % ngx;
+  const int cx = P.PL + P.s0c; // shared column of store column 0 (16-byte aligned)
+  const bool vec = (P.nx & 3) == 0; // exchange rows move as 16-byte vectors
+  int cur = 0;
+  int done = 0, blk = 0;
+  while (done < P.steps) {
+    const int kk = min(P.K, P.steps - done);
+    for (int s = 0; s < kk; ++s) {
+      const int ylo = max(0, r0 - (kk - 1 - s) * R), yhi = min(P.ny, r1 + (kk - 1 - s) * R);
+      const T *in = tile(cur);
+      T *out = tile(cur ^ 1);
+      // work items: 4 points in each of two consecutive rows (y, y+1), row-pair-major from
+      // (ylo, 0); the two rows share their column neighbours' loads (2R+6 LDS.128 for 8
+      // points instead of 2(2R+3)).  This thread's walk needs no division.
+      int pr = gy0, gx = gx0;
+      for (; ylo + 2 * pr < yhi;
+           gx += dgx, pr += dgy + (gx >= ngx ? 1 : 0), gx -= gx >= ngx ? ngx : 0) {
+        const int y = ylo + 2 * pr, x0 = gx * 4;
+        const bool two = y + 1 < yhi;
+        const int i = P.s0r + y - lo; // tile row of y
+        const T *row = in + size_t(i) * P.SP + cx + x0;
+        V4<T> cen[2 * R + 2]; // centres of rows y-R .. y+1+R
+#pragma unroll
+        for (int d = 0; d < 2 * R + 2; ++d)
+          if (d != 2 * R + 1 || two)
+            cen[d] = ld4(row + (d - R) * P.SP);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two)
+            break;
+          const V4<T> L = ld4(row + h * P.SP - 4), Rr = ld4(row + h * P.SP + 4);
+          const V4<T> &Cc = cen[R + h];
+          V4<T> o;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const T cc = Cc.v[j];
+            T acc = mul_(cc, P.w0);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const int k = Taps<NT>::k(t);
+              acc = add_(acc, mul_(add_(cen[R + h + k].v[j], cen[R + h - k].v[j]), P.wz[t]));
+            }
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const int k = Taps<NT>::k(t);
+              const int ip = 4 + j + k, im = 4 + j - k; // window [L | Cc | Rr]
+              const T xp = ip < 4 ? L.v[ip & 3] : (ip < 8 ? Cc.v[ip & 3] : Rr.v[ip & 3]);
+              const T xm = im < 4 ? L.v[im & 3] : (im < 8 ? Cc.v[im & 3] : Rr.v[im & 3]);
+              acc = add_(acc, mul_(add_(xp, xm), P.wx[t]));
+            }
+            o.v[j] = add_(cc, mul_(acc, P.scale));
+          }
+          T *dst = out + size_t(i + h) * P.SP + cx + x0;
+          if (x0 + 4 <= P.nx) {
+            st4(dst, o);
+          } else { // the ring columns right of the store box stay untouched
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (x0 + j < P.nx)
+                dst[j] = o.v[j];
+          }
+        }
+      }
+      __syncthreads();
+      cur ^= 1;
+    }
+    done += kk;
+    if (done >= P.steps)
+      break;
+    // ---- exchange the E boundary rows of the current level with the band neighbours ----
+    const int par = blk & 1;
+    const size_t slot = size_t(E) * P.nx;
+    if constexpr (sizeof(T) == 4) {
+      // f32: every value travels in a 64-bit word with its block tag in the high half, so the
+      // word itself is the flag (single-copy atomic): no fence, no flag round trip.  Slot
+      // reuse two blocks later is safe: a CTA overwrites slot `par` only after it has read the
+      // neighbour's NEXT block, which the neighbour computed from this one.
+      using W64 = unsigned long long;
+      W64 *xw = reinterpret_cast<W64 *>(P.xbuf);
+      const W64 tg = W64(P.tag0 + unsigned(blk) + 1u) << 32;
+      W64 *mine = xw + (size_t(par) * G + c) * 2 * slot;
+      const T *t = tile(cur);
+      for (int r = 0; r < 2 * E; ++r) {
+        const int y = r < E ? r0 + r : r1 - 2 * E + r;
+        const T *src = t + size_t(P.s0r + y - lo) * P.SP + cx;
+        for (int x = tid; x < P.nx; x += kResThreads) {
+          const W64 w = tg | __float_as_uint(src[x]);
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(mine + size_t(r) * P.nx + x),
+                       "l"(w)
+                       : "memory");
+        }
+      }
+      T *tw = tile(cur);
+      for (int r = 0; r < 2 * E; ++r) {
+        const bool top = r < E;
+        const int nb = top ? c - 1 : c + 1;
+        if (nb < 0 || nb >= G)
+          continue;
+        const W64 *src = xw + (size_t(par) * G + nb) * 2 * slot + (top ? slot : 0) +
+                         size_t(top ? r : r - E) * P.nx;
+        const int y = top ? r0 - E + r : r1 + r - E;
+        T *dst = tw + size_t(P.s0r + y - lo) * P.SP + cx;
+        for (int x = tid; x < P.nx; x += kResThreads) {
+          W64 w;
+          do {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(src + x)
+                         : "memory");
+          } while ((w & ~0xffffffffull) != tg);
+          dst[x] = __uint_as_float(unsigned(w));
+        }
+      }
+      __syncthreads();
+      ++blk;
+      continue;
+    }
+    T *mine = P.xbuf + (size_t(par) * G + c) * 2 * slot;
+    const T *t = tile(cur);
+    if (vec) {
+      const int nv = P.nx / 4;
+      for (int k = tid; k < 2 * E * nv; k += kResThreads) {
+        const int r = k / nv, v = k - r * nv; // r: slot row (side * E + j)
+        const int y = r < E ? r0 + r : r1 - 2 * E + r;
+        st4(mine + size_t(r) * P.nx + 4 * v, ld4(t + size_t(P.s0r + y - lo) * P.SP + cx + 4 * v));
+      }
+    } else {
+      for (int k = tid; k < 2 * E * P.nx; k += kResThreads) {
+        const int side = k / (E * P.nx), j = (k / P.nx) % E, x = k % P.nx;
+        const int y = side == 0 ? r0 + j : r1 - E + j;
+        mine[k] = t[size_t(P.s0r + y - lo) * P.SP + cx + x];
+      }
+    }
+    __syncthreads();
+    const unsigned long long want = P.epoch + blk + 1;
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(P.flags + c), "l"(want)
+                   : "memory");
+      for (int nb = c - 1; nb <= c + 1; nb += 2) {
+        if (nb < 0 || nb >= G)
+          continue;
+        unsigned long long v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.flags + nb)
+                       : "memory");
+        } while (v < want);
+      }
+    }
+    __syncthreads();
+    T *tw = tile(cur);
+    if (vec) {
+      const int nv = P.nx / 4;
+      for (int k = tid; k < 2 * E * nv; k += kResThreads) {
+        const int r = k / nv, v = k - r * nv;
+        // rows [r0-E, r0) = the upper neighbour's last E rows; [r1, r1+E) = the lower one's first
+        const bool top = r < E;
+        const int nb = top ? c - 1 : c + 1;
+        if (nb < 0 || nb >= G)
+          continue;
+        const T *src = P.xbuf + (size_t(par) * G + nb) * 2 * slot + (top ? slot : 0) +
+                       size_t(top ? r : r - E) * P.nx + 4 * v;
+        const int y = top ? r0 - E + r : r1 + r - E;
+        V4<T> w;
+        if constexpr (sizeof(T) == 4) {
+          const float4 a = __ldcg(reinterpret_cast<const float4 *>(src));
+          w = {{a.x, a.y, a.z, a.w}};
+        } else {
+          const double2 a = __ldcg(reinterpret_cast<const double2 *>(src));
+          const double2 b = __ldcg(reinterpret_cast<const double2 *>(src) + 1);
+          w = {{a.x, a.y, b.x, b.y}};
+        }
+        st4(tw + size_t(P.s0r + y - lo) * P.SP + cx + 4 * v, w);
+      }
+    } else {
+      for (int k = tid; k < 2 * E * P.nx; k += kResThreads) {
+        const int side = k / (E * P.nx), j = (k / P.nx) % E, x = k % P.nx;
+        const int nb = side == 0 ? c - 1 : c + 1;
+        if (nb < 0 || nb >= G)
+          continue;
+        const T *src = P.xbuf + (size_t(par) * G + nb) * 2 * slot;
+        const int y = side == 0 ? r0 - E + j : r1 + j;
+        const T v = __ldcg(src + (side == 0 ? slot : 0) + size_t(j) * P.nx + x);
+        tw[size_t(P.s0r + y - lo) * P.SP + cx + x] = v;
+      }
+    }
+    __syncthreads();
+    ++blk;
+  }
+
+  // ---- write the band's store rows of both tiles back ----
+  for (int b = 0; b < 2; ++b) {
+    const T *t = tile(b);
+    T *g = b ? P.buf[1] : P.buf[0];
+    for (int64_t k = tid; k < int64_t(r1 - r0) * P.nx; k += kResThreads) {
+      const int y = r0 + int(k / P.nx), x = int(k % P.nx);
+      g[int64_t(P.s0r + y) * P.pitch + P.col0 + P.s0c + x] =
+          t[size_t(P.s0r + y - lo) * P.SP + cx + x];
+    }
+  }
+}
+
+struct ResGeometry {
+  int G = 0, K = 0, E = 0, maxRows = 0, SP = 0, PL = 0;
+  size_t smem = 0;
+};
+
+int numSMs() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
+// Band count, steps per exchange and shared-memory footprint; false if it does not fit.
+bool geometry(const ResLaunch &L, ResGeometry &g) {
+  const int R = L.spec->radius, es = L.dtype == HG_F32 ? 4 : 8;
+  const int W = int(L.lay.shape[1]);
+  const int s0c = int(L.start[1]);
+  const int ny = int(L.ext[0]);
+  g.PL = (4 - s0c % 4) % 4;
+  if (g.PL + s0c < 4)
+    g.PL += 4;
+  g.SP = (g.PL + W + 8 + 3) / 4 * 4;
+  const size_t cap = 227 * 1024;
+  static const int kMax = [] { // tuning experiments only
+    const char *e = std::getenv("HG_RES_K"); // default 2: best of 1/2/4/6/8 (r1_sweeps.md)
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  static const int gMax = [] { // tuning experiments only
+    const char *e = std::getenv("HG_RES_G");
+    return e ? std::max(1, std::atoi(e)) : 1 << 30;
+  }();
+  for (int G = std::min(std::min(numSMs(), gMax), ny); G >= 1; --G) {
+    const int minRows = ny / G, maxRows = (ny + G - 1) / G;
+    int K = std::min(kMax, minRows / R); // steps per exchange
+    if (K < 1)
+      continue;
+    while (K > 1 && size_t(2) * (maxRows + 2 * K * R) * g.SP * es > cap)
+      --K;
+    const size_t smem = size_t(2) * (maxRows + 2 * K * R) * g.SP * es;
+    if (smem > cap)
+      return false; // fewer bands only grow the tiles
+    g.G = G;
+    g.K = K;
+    g.E = K * R;
+    g.maxRows = maxRows;
+    g.smem = smem;
+    return true;
+  }
+  return false;
+}
+
+template <typename T, int NT> int launchResT(const ResLaunch &L, const ResGeometry &g,
+                                             cudaStream_t st) {
+  auto kern = residentKernel<T, NT>;
+  static std::mutex mu;
+  static unsigned long long doneMask = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(doneMask & (1ull << (dev & 63)))) {
+      cudaError_t e =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess)
+        return cudaErrRes(e, "cudaFuncSetAttribute(resident)");
+      doneMask |= 1ull << (dev & 63);
+    }
+  }
+  const StarSpec &s = *L.spec;
+  ResParams<T> P{};
+  P.buf[0] = static_cast<T *>(L.in);
+  P.buf[1] = static_cast<T *>(L.out);
+  P.xbuf = static_cast<T *>(L.xbuf);
+  P.flags = L.flags;
+  P.epoch = L.epoch;
+  P.tag0 = L.tag0;
+  P.pitch = L.lay.pitch;
+  P.col0 = L.lay.col0;
+  P.H = int(L.lay.shape[0]);
+  P.W = int(L.lay.shape[1]);
+  P.s0r = int(L.start[0]);
+  P.s0c = int(L.start[1]);
+  P.ny = int(L.ext[0]);
+  P.nx = int(L.ext[1]);
+  P.steps = int(L.steps);
+  P.K = g.K;
+  P.E = g.E;
+  P.maxRows = g.maxRows;
+  P.SP = g.SP;
+  P.PL = g.PL;
+  P.w0 = fromBits<T>(s.w0);
+  for (int t = 0; t < 3; ++t) {
+    P.wz[t] = fromBits<T>(s.w[0][t]);
+    P.wx[t] = fromBits<T>(s.w[1][t]);
+  }
+  P.scale = fromBits<T>(s.scale);
+  void *args[] = {&P};
+  return cudaErrRes(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern),
+                                                dim3(g.G), dim3(kResThreads), args, g.smem, st),
+                    "resident kernel launch");
+}
+
+} // namespace
+
+bool residentSupported(const ResLaunch &L, size_t *xbufBytes, int *ctas) {
+  const StarSpec &s = *L.spec;
+  if (s.kind != kHeat || s.rank != 2 || L.ext[0] <= 0 || L.ext[1] <= 0)
+    return false;
+  ResGeometry g;
+  if (!geometry(L, g))
+    return false;
+  const int es = L.dtype == HG_F32 ? 4 : 8;
+  if (xbufBytes) // f32 moves tagged 64-bit words
+    *xbufBytes = size_t(2) * g.G * 2 * g.E * size_t(L.ext[1]) * 8;
+  (void)es;
+  if (ctas)
+    *ctas = g.G;
+  return true;
+}
+
+int launchResident(const ResLaunch &L, cudaStream_t st) {
+  ResGeometry g;
+  if (!geometry(L, g))
+    return setError(HG_EUNSUPPORTED, "resident 2D kernel: fields do not fit in shared memory");
+  const int nt = L.spec->ntaps;
+  if (L.dtype == HG_F32)
+    return nt == 1 ? launchResT<float, 1>(L, g, st)
+                   : nt == 2 ? launchResT<float, 2>(L, g, st) : launchResT<float, 3>(L, g, st);
+  return nt == 1 ? launchResT<double, 1>(L, g, st)
+                 : nt == 2 ? launchResT<double, 2>(L, g, st) : launchResT<double, 3>(L, g, st);
+}
+
+} // namespace hg

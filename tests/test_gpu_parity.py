@@ -36,7 +36,7 @@ def test_serial_cases_bitwise(golden):
     for c in _serial(golden):
         prog = program_from_json(c["program"])
         init, fin, perm, name = _plan_run(prog, c["T"])
-        seen.add(name)
+        seen.add(name.replace("+resident", ""))
         assert [fp_hex(a) for a in init] == c["init_fp"], case_id(c)
         assert [fp_hex(a) for a in fin] == c["final_fp"], (case_id(c), name)
     # both families and every tap radius were exercised
@@ -44,11 +44,16 @@ def test_serial_cases_bitwise(golden):
             "star3d_r4_heat_f64", "generic1d_f32"} <= seen
 
 
-def test_config1_full_run_bitwise(golden):
+@pytest.mark.parametrize("path", ["resident", "star"])
+def test_config1_full_run_bitwise(golden, monkeypatch, path):
+    # BASELINE config 1 end to end against the reference's own fingerprints: the whole run in
+    # one shared-memory-resident launch (default) and step by step through the star kernel
+    if path == "star":
+        monkeypatch.setenv("HG_NO_RESIDENT", "1")
     (c,) = _serial(golden, big=True)
     prog = program_from_json(c["program"])
     _, fin, _, name = _plan_run(prog, c["T"])
-    assert name == "star2d_r1_heat_f32"
+    assert name == "star2d_r1_heat_f32" + ("+resident" if path == "resident" else "")
     assert [fp_hex(a) for a in fin] == ["b11e8dddf9e8c23c", "34a5556efc0dfea0"]
 
 
@@ -446,3 +451,37 @@ def test_host_transfers_and_live_upload(port, pinned, spec, T):
     assert perm == perm_o
     for g, p in zip(outs, perm_o):
         assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
+
+
+@pytest.mark.parametrize("spec,T", [
+    (("heat", 2, 1024, 2), 1), (("heat", 2, 1024, 2), 7), (("heat", 2, 1024, 2), 13),
+    (("heat", 2, 1000, 4), 9), (("heat", 2, 777, 8), 6), (("heat", 2, 37, 2), 11),
+    (("heat", 2, 300, 8), 3), (("heat", 2, 5, 2), 4)])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_resident_2d_bitwise(port, spec, T, dtype):
+    # the shared-memory-resident whole-run kernel: bands, temporal blocks of K steps with the
+    # boundary-row exchange between them, ragged last blocks and row/column tails, both
+    # buffers' halo rings -- bitwise against the oracle, and split calls equal one call
+    prog = hg.build_kernel(hg.KernelSpec(*spec, dtype))
+    arrays = port.initial_fields(prog)
+    perm_o = port.run(prog, arrays, T)
+    plan = hg.Plan(prog)
+    try:
+        plan.init_fields()
+        assert plan.kernel_name.endswith("+resident"), plan.kernel_name
+        plan.run(T)
+        perm, _ = plan.binding()
+        got = [plan.download(p) for p in perm]
+        plan.init_fields()
+        plan.reset_binding()
+        plan.run(T // 2)
+        plan.run(T - T // 2)
+        perm2, _ = plan.binding()
+        got2 = [plan.download(p) for p in perm2]
+    finally:
+        plan.close()
+    assert perm == perm_o == perm2
+    u = np.uint32 if dtype == "f32" else np.uint64
+    for g, g2, p in zip(got, got2, perm_o):
+        assert np.array_equal(g.view(u), arrays[p].view(u))
+        assert np.array_equal(g2.view(u), arrays[p].view(u))
