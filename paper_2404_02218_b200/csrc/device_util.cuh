@@ -112,6 +112,28 @@ __device__ __forceinline__ void tmaLoad3d(void *dst, const CUtensorMap *map, uin
                : "memory");
 }
 
+// The same load with an L2 eviction-priority policy (createpolicy): planes the next z-chunk
+// of the same column will re-read are kept (evict_last); planes read for the last time go
+// first (evict_first).
+__device__ __forceinline__ uint64_t l2PolicyEvictLast() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2PolicyEvictFirst() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tmaLoad3dHint(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                              int c0, int c1, int c2, uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+               ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smemAddr(dst)),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+               "r"(smemAddr(bar)), "l"(policy)
+               : "memory");
+}
+
 // Calls f(mb + U, integral_constant<U>) for U = 0, 1, ... while it returns true.
 template <typename F, int... Us>
 __device__ __forceinline__ void unrolled(F &f, int mb, std::integer_sequence<int, Us...>) {

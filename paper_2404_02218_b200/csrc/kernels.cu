@@ -109,6 +109,10 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
 #ifndef HG_PACK
 #define HG_PACK 0
 #endif
+// L2 eviction hints on the z-halo planes shared by consecutive chunks (A/B: HG_L2HINT=0)
+#ifndef HG_L2HINT
+#define HG_L2HINT 1
+#endif
 template <typename T> constexpr bool kPackF32 = HG_PACK && std::is_same<T, float>::value;
 
 template <typename T> struct StarParams {
@@ -266,13 +270,26 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       const int z0 = P.zs + zb - R;
       constexpr uint32_t curBytes = uint32_t(C::STAGE * sizeof(T));
       constexpr uint32_t prevBytes = uint32_t(C::PSTAGE * sizeof(T));
+      // z-halo planes shared with the neighbouring chunks of this column: the last 2R planes
+      // this chunk loads are the first 2R of the next chunk -- keep them in L2 (evict_last)
+      // until that chunk has read them (evict_first), instead of fetching them from HBM twice
+      // (heat only: ncu DRAM reads 4.90 -> 4.70 GB per 1024^3 step; the wave kernel, whose
+      // prev box shares the stage, measured 4% slower with the hints -- profiles/r1_sweeps.md)
+      const bool hintL2 = HG_L2HINT && !C::WAVE && P.nchunks > 1;
+      const uint64_t keep = hintL2 ? l2PolicyEvictLast() : 0;
+      const uint64_t drop = hintL2 ? l2PolicyEvictFirst() : 0;
       for (int i = 0; i < n + 2 * R; ++i) {
         const int s = i % NS;
         if (i >= NS)
           mbarWait(&empty[s], uint32_t((i / NS - 1) & 1));
         const bool wantPrev = C::WAVE && i >= R && i < n + R;
         mbarExpectTx(&full[s], curBytes + (wantPrev ? prevBytes : 0u));
-        tmaLoad3d(stages + size_t(s) * C::SSTRIDE, &tmCur, &full[s], cx, cy, z0 + i);
+        if (hintL2 && i >= n && zb + n < P.nz)
+          tmaLoad3dHint(stages + size_t(s) * C::SSTRIDE, &tmCur, &full[s], cx, cy, z0 + i, keep);
+        else if (hintL2 && i < 2 * R && zb > 0)
+          tmaLoad3dHint(stages + size_t(s) * C::SSTRIDE, &tmCur, &full[s], cx, cy, z0 + i, drop);
+        else
+          tmaLoad3d(stages + size_t(s) * C::SSTRIDE, &tmCur, &full[s], cx, cy, z0 + i);
         if (wantPrev)
           tmaLoad3d(pstages + size_t(s) * C::PSTAGE, &tmPrev, &full[s], cx + C::PADX,
                     RANK == 3 ? P.ys + yb : 0, z0 + i);
