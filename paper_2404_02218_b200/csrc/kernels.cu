@@ -526,9 +526,13 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
             continue;
         }
         T *dst = P.peer[d] + e0 + P.pdelta[d];
+        // 16-byte copies only when the receive position keeps the 16-byte alignment of the
+        // source: an x face between ranks whose core width is not a multiple of 16 bytes
+        // (e.g. 50 points per rank) shifts it (misaligned-address fault otherwise)
+        const bool vec = (P.pdelta[d] * int64_t(sizeof(T))) % 16 == 0;
         for (int m = m0; m < m1; ++m) {
           const int64_t off = int64_t(m) * P.plane;
-          if (jmask == 0xF && xrem >= 4) {
+          if (vec && jmask == 0xF && xrem >= 4) {
             st4(dst + off, ld4(src + off));
           } else {
             for (int j = 0; j < 4; ++j)
