@@ -236,7 +236,11 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
     s << "((double2 *)q)[0] = make_double2(r.v[0], r.v[1]); ((double2 *)q)[1] = "
          "make_double2(r.v[2], r.v[3]); ";
   s << "}\n";
-  s << "extern \"C\" __global__ void __launch_bounds__(" << K.nthreads
+  static const int minBlocks = [] { // tuning experiments only
+    const char *e = std::getenv("HG_JIT_MINB");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  s << "extern \"C\" __global__ void __launch_bounds__(" << K.nthreads << ", " << minBlocks
     << ") hg_apply(const __grid_constant__ P_t P) {\n";
   s << "  constexpr int O = " << O << ", RZ = " << rz << ", RY = " << ry << ", NS = " << K.ns
     << ", TXT = " << K.txt << ", TX = " << K.tx << ", TY = " << K.ty << ", CW = " << cw
