@@ -123,7 +123,11 @@ def _ncu_traffic(workload):
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        e = d.get(workload, {})
+        if "dram_bytes_per_launch" not in e:
+            return None
+        # a whole-run launch (resident kernel) is reported per step, like `achieved`
+        return e["dram_bytes_per_launch"] / e.get("steps_per_launch", 1)
     except Exception:
         return None
 
@@ -436,7 +440,8 @@ def run_ours(args):
     bpp = WORKLOADS[args.workload]["bpp"]
     achieved = bpp * core_local / (k_ms / 1e3) / 1e9
     traffic = _ncu_traffic({"heat3d_weak": "r1_heat3d_so4_1024", "pw_advection": "r1_pw_advection_128x512x512",
-                            "wave3d_1024": "r1_wave3d_so8_1024"}.get(args.workload, ""))
+                            "wave3d_1024": "r1_wave3d_so8_1024",
+                            "heat2d_1024": "r1_resident_heat2d_1024"}.get(args.workload, ""))
 
     # end to end through the public API with HOST buffers: upload -> T steps -> download
     e2e = None

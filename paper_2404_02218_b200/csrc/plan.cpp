@@ -8,6 +8,7 @@
 #include <exception>
 #include <map>
 #include <mutex>
+#include <thread>
 
 namespace hg {
 
@@ -688,6 +689,130 @@ static void *mappedHost(void *host) {
   return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
 }
 
+// Pageable host memory: a pinned two-buffer staging ring per device.  The host side of each
+// chunk is a multi-threaded memcpy (one core's memcpy runs at ~10 GB/s, below PCIe), the
+// device side the zero-copy kernel (uploads) or a pitched copy-engine copy (downloads), and
+// chunk k's transfer overlaps chunk k+1's (or k-1's) host copy.
+namespace {
+constexpr size_t kStageBytes = size_t(128) << 20;
+
+struct Staging {
+  std::mutex mu;
+  void *buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+Staging *stagingFor(int device) {
+  static std::mutex mu;
+  static std::map<int, Staging *> all; // process lifetime, like the CUDA context
+  std::lock_guard<std::mutex> lk(mu);
+  Staging *&st = all[device];
+  if (!st)
+    st = new Staging;
+  return st;
+}
+
+int ensureStaging(Staging &st) {
+  for (int i = 0; i < 2; ++i) {
+    if (!st.buf[i]) {
+      int rc = cudaCheck(cudaHostAlloc(&st.buf[i], kStageBytes, cudaHostAllocDefault),
+                         "cudaHostAlloc(staging)");
+      if (rc)
+        return rc;
+    }
+    if (!st.ev[i]) {
+      int rc = cudaCheck(cudaEventCreateWithFlags(&st.ev[i], cudaEventDisableTiming),
+                         "cudaEventCreate(staging)");
+      if (rc)
+        return rc;
+    }
+  }
+  return HG_OK;
+}
+
+void parallelCopy(void *dst, const void *src, size_t n) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>(std::min<size_t>(hw, 8), std::max<size_t>(1, n >> 23));
+  if (nt <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  const size_t per = (n + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (size_t t = 1; t < nt; ++t) {
+    const size_t o = t * per;
+    if (o >= n)
+      break;
+    th.emplace_back([=] {
+      std::memcpy(static_cast<char *>(dst) + o, static_cast<const char *>(src) + o,
+                  std::min(per, n - o));
+    });
+  }
+  std::memcpy(dst, src, std::min(per, n));
+  for (auto &t : th)
+    t.join();
+}
+
+int stagedCopy(hg_plan *p, int b, char *host, bool up, cudaStream_t s) {
+  const Layout &L = p->lay[static_cast<size_t>(b)];
+  Staging &sg = *stagingFor(p->device);
+  std::lock_guard<std::mutex> lk(sg.mu);
+  int rc = ensureStaging(sg);
+  if (rc)
+    return rc;
+  const size_t rowBytes = static_cast<size_t>(L.shape[L.rank - 1]) * L.es;
+  const int64_t rpc = std::max<int64_t>(1, static_cast<int64_t>(kStageBytes / rowBytes));
+  char *dev = static_cast<char *>(p->dptr[static_cast<size_t>(b)]);
+  const size_t dp = static_cast<size_t>(L.pitch) * L.es;
+  DevLayout v = devLayout(L); // a chunk of rows viewed as a 2D field of its own
+  v.rank = 2;
+  v.shape[1] = L.shape[L.rank - 1];
+  v.lb[0] = v.lb[1] = 0;
+  int64_t prevR = 0, prevN = 0;
+  int k = 0;
+  for (int64_t r = 0; r < L.rows; r += rpc, ++k) {
+    const int64_t n = std::min(rpc, L.rows - r);
+    const int sb = k & 1;
+    if (up) {
+      // the transfer that last read this staging buffer (this call or the previous one)
+      rc = cudaCheck(cudaEventSynchronize(sg.ev[sb]), "staging wait");
+      if (rc)
+        return rc;
+      parallelCopy(sg.buf[sb], host + r * rowBytes, static_cast<size_t>(n) * rowBytes);
+      v.shape[0] = n;
+      rc = launchHostXfer(dev + static_cast<size_t>(r) * dp, v, sg.buf[sb], 1, nullptr, nullptr,
+                          s);
+      ++p->launches;
+    } else {
+      rc = cudaCheck(cudaMemcpy2DAsync(sg.buf[sb], rowBytes,
+                                       dev + static_cast<size_t>(r) * dp + L.col0 * L.es, dp,
+                                       rowBytes, static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                                       s),
+                     "download");
+      if (!rc && k > 0) { // drain the previous chunk while this one is in flight
+        rc = cudaCheck(cudaEventSynchronize(sg.ev[sb ^ 1]), "staging wait");
+        if (!rc)
+          parallelCopy(host + prevR * rowBytes, sg.buf[sb ^ 1],
+                       static_cast<size_t>(prevN) * rowBytes);
+      }
+    }
+    if (!rc)
+      rc = cudaCheck(cudaEventRecord(sg.ev[sb], s), "staging event");
+    if (rc)
+      return rc;
+    prevR = r;
+    prevN = n;
+  }
+  if (!up && k > 0) {
+    rc = cudaCheck(cudaEventSynchronize(sg.ev[(k - 1) & 1]), "staging wait");
+    if (!rc)
+      parallelCopy(host + prevR * rowBytes, sg.buf[(k - 1) & 1],
+                   static_cast<size_t>(prevN) * rowBytes);
+  }
+  return rc;
+}
+} // namespace
+
 // skip_lo/hi: raw box of buffer b not to move (uploads only; null = move everything)
 static int copyField(hg_plan *p, int b, void *host, size_t bytes, void *stream, bool up,
                      const int64_t *skip_lo, const int64_t *skip_hi) {
@@ -713,6 +838,12 @@ static int copyField(hg_plan *p, int b, void *host, size_t bytes, void *stream, 
       st = cudaCheck(cudaStreamSynchronize(s), "download");
     return st;
   }
+  // pageable memory, large fields: through the pinned staging ring
+  static const bool noStage = std::getenv("HG_NO_STAGING") != nullptr; // A/B only
+  if (!noStage && !(force && force[0] == 'c') &&
+      static_cast<size_t>(L.logicalCount()) * L.es >= (size_t(32) << 20) &&
+      !mappedHost(host))
+    return stagedCopy(p, b, static_cast<char *>(host), up, s);
   // pageable memory: the copy engines, one pitched copy of the whole field
   const size_t w = static_cast<size_t>(L.shape[L.rank - 1]) * L.es;
   char *dev = static_cast<char *>(p->dptr[static_cast<size_t>(b)]) + L.col0 * L.es;

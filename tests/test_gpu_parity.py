@@ -485,3 +485,25 @@ def test_resident_2d_bitwise(port, spec, T, dtype):
     for g, g2, p in zip(got, got2, perm_o):
         assert np.array_equal(g.view(u), arrays[p].view(u))
         assert np.array_equal(g2.view(u), arrays[p].view(u))
+
+
+def test_pageable_staged_transfers(port):
+    # fields >= 32 MB in pageable host memory go through the pinned staging ring (chunks of
+    # rows, multi-threaded host copies overlapped with the transfers): round trip and a run
+    prog = hg.build_kernel(hg.KernelSpec("heat", 3, 300, 4, "f32"))  # 304^3 f32 = 112 MB
+    arrays = port.initial_fields(prog)
+    plan = hg.Plan(prog)
+    try:
+        for i, a in enumerate(arrays):
+            plan.upload(i, a.copy(), live=(i == 1))
+        back = plan.download(0)
+        assert np.array_equal(back.view(np.uint32), arrays[0].view(np.uint32))
+        plan.run(2)
+        perm, _ = plan.binding()
+        got = [plan.download(p) for p in perm]
+    finally:
+        plan.close()
+    perm_o = port.run(prog, arrays, 2)
+    assert perm == perm_o
+    for g, p in zip(got, perm_o):
+        assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))

@@ -46,8 +46,8 @@ def main():
     print(f"plan up live (field 1: halo shell only) "
           f"{rate(lambda: plan.upload(1, host.numpy(), live=True), nb):.1f} GB/s-equivalent")
     pageable = host.numpy().copy()
-    print(f"plan up pageable {rate(lambda: plan.upload(0, pageable), nb, reps=1):.1f} GB/s")
-    print(f"plan down pageable {rate(lambda: plan.download(0, pageable), nb, reps=1):.1f} GB/s")
+    print(f"plan up pageable {rate(lambda: plan.upload(0, pageable), nb, reps=2):.1f} GB/s")
+    print(f"plan down pageable {rate(lambda: plan.download(0, pageable), nb, reps=2):.1f} GB/s")
     # chunked flat copies
     for mb in (64, 256):
         ch = mb << 20
