@@ -167,8 +167,16 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   }
   K.rz = rz;
   K.ry = ry;
-  K.txt = r == 3 ? 16 : 32;
-  K.tyt = r == 3 ? 16 : 1;
+  static const int envTxt = [] { // tuning experiments only: threads along x (4 points each)
+    const char *e = std::getenv("HG_JIT_TXT");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int envTyt = [] { // tuning experiments only: rows per tile
+    const char *e = std::getenv("HG_JIT_TYT");
+    return e ? std::atoi(e) : 0;
+  }();
+  K.txt = r == 3 ? (envTxt == 32 ? 32 : 16) : 32;
+  K.tyt = r == 3 ? (envTyt > 0 && (envTyt * K.txt) % 32 == 0 ? envTyt : 16) : 1;
   K.tx = K.txt * 4;
   K.ty = K.tyt;
   const int O = p.noperands;
