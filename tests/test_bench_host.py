@@ -1,0 +1,44 @@
+"""CPU checks of bench.py's host-side bookkeeping (no GPU): the e2e byte counts follow the
+programs (hg_plan_upload_live skips exactly the output slot's store box), the config fields
+describe each BASELINE workload, and the reference arm runs on every core it is given."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+import paper_2404_02218_b200 as hg
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import bench  # noqa: E402
+
+
+def test_dead_on_arrival_bytes_follow_the_store_boxes():
+    heat = hg.build_kernel(hg.KernelSpec("heat", 3, 64, 4, "f32"))
+    assert bench.dead_on_arrival_bytes(heat, 4) == 64 ** 3 * 4      # u_out's core only
+    wave = hg.build_kernel(hg.KernelSpec("wave", 3, 40, 8, "f32"))
+    assert bench.dead_on_arrival_bytes(wave, 4) == 40 ** 3 * 4      # next's core only
+    pw = hg.Program.pw_advection(16, 24, 40)
+    assert bench.dead_on_arrival_bytes(pw, 4) == 3 * 16 * 24 * 40 * 4  # su, sv, sw cores
+
+
+@pytest.mark.parametrize("workload,core,halo", [
+    ("heat3d_512", [512, 512, 512], 2), ("wave3d_1024", [1024, 1024, 1024], 4),
+    ("pw_advection", [128, 512, 512], 1), ("heat2d_1024", [1024, 1024], 1)])
+def test_workload_config_fields(workload, core, halo):
+    prog = bench.WORKLOADS[workload]["build"](hg)
+    assert bench.core_extents(prog) == core
+    assert bench.halo_width(prog) == halo
+    assert bench.plan_bytes(prog) > 0
+
+
+def test_reference_arm_uses_the_given_cores():
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "1", "--ref-extent", "24", "--ref-procs",
+                        "2"], capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["cpu_baseline"]["cores"] == 2
+    assert line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
