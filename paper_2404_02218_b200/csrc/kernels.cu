@@ -93,14 +93,20 @@ int cudaErr(cudaError_t e, const char *what) {
 // would exceed the 227 KB of shared memory at 8 bytes per element).
 template <int RANK, int R, int GEO = 0, int ES = 4> struct StarGeom;
 template <int R, int ES> struct StarGeom<3, R, 1, ES> {
-  static constexpr int TXT = 32, TYT = 12;
+  static constexpr int TXT = 32, TYT = 12, PTS = 4;
+};
+// GEO 2: the wide tile with 8 x-points per thread (half the threads; per-plane overhead --
+// waits, stage bookkeeping, addressing -- amortised over twice the points)
+template <int R, int ES> struct StarGeom<3, R, 2, ES> {
+  static constexpr int TXT = 16, TYT = 12, PTS = 8;
 };
 template <int R, int ES> struct StarGeom<3, R, 0, ES> {
+  static constexpr int PTS = 4;
   static constexpr int TXT = R >= 4 ? HG_TXT_R4 : HG_TXT_R2;
   static constexpr int TYT = R >= 4 ? (ES == 8 ? 16 : HG_TYT_R4) : HG_TYT_R2;
 };
 template <int R, int ES> struct StarGeom<2, R, 0, ES> {
-  static constexpr int TXT = 32, TYT = 1;
+  static constexpr int TXT = 32, TYT = 1, PTS = 4;
 };
 
 // f32 star arithmetic on packed f32x2 pairs: bit-exact, but measured 4-8% slower than the
@@ -108,6 +114,9 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
 // product builds the scalar form; HG_PACK=1 builds the packed one for A/B
 #ifndef HG_PACK
 #define HG_PACK 0
+#endif
+#ifndef HG_MINB_G2
+#define HG_MINB_G2 3
 #endif
 // L2 eviction hints on the z-halo planes shared by consecutive chunks (A/B: HG_L2HINT=0)
 #ifndef HG_L2HINT
@@ -154,7 +163,8 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int RY = RANK == 3 ? R : 0;
   static constexpr int TXT = StarGeom<RANK, R, GEO, int(sizeof(T))>::TXT,
                        TYT = StarGeom<RANK, R, GEO, int(sizeof(T))>::TYT;
-  static constexpr int TX = TXT * 4, TY = TYT;
+  static constexpr int PTS = StarGeom<RANK, R, GEO, int(sizeof(T))>::PTS; // x-points/thread
+  static constexpr int TX = TXT * PTS, TY = TYT;
   static constexpr int PADX = 4;
   static constexpr int CW = TX + 2 * PADX;
   static constexpr int ROWS = TY + 2 * RY;
@@ -163,7 +173,8 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int NTHREADS = NCONS + 32;
   // CTAs per SM the register budget must allow (f32 3D: 3 for r<=2, 2 for r=4)
   static constexpr int MINB =
-      GEO == 1 ? 2 : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
+      GEO == 1 ? 2 : GEO == 2 ? HG_MINB_G2
+                   : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
   static constexpr int DEPTH =
       RANK == 3 ? (R <= 2 ? HG_DEPTH3 : (sizeof(T) == 8 ? 5 : HG_DEPTH3W)) : HG_DEPTH2;
   static constexpr int NS = R + 1 + DEPTH;
@@ -301,9 +312,10 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   // ---------------- consumers ----------------
   const int tx = tid % C::TXT, ty = tid / C::TXT;
   const int lane = tid & 31;
-  const int x0 = tx * 4;
+  constexpr int PTS = C::PTS, NV = PTS / 4; // x-points per thread, 4-vectors per row
+  const int x0 = tx * PTS;
   const int rowOwn = (ty + RY) * C::CW;   // own row in a stage
-  T q[Q][4];
+  T q[Q][PTS];
 
   auto release = [&](int s) {
     __syncwarp();
@@ -316,10 +328,13 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   for (int i = 0; i < 2 * R; ++i) {
     const int s = i % NS;
     mbarWait(&full[s], uint32_t((i / NS) & 1));
-    V4<T> c = ld4(stages + size_t(s) * C::SSTRIDE + rowOwn + C::PADX + x0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      q[i][j] = c.v[j];
+    for (int h = 0; h < NV; ++h) {
+      V4<T> c = ld4(stages + size_t(s) * C::SSTRIDE + rowOwn + C::PADX + x0 + 4 * h);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        q[i][4 * h + j] = c.v[j];
+    }
   }
 
   const bool yok = RANK == 2 || (yb + ty < P.ny);
@@ -354,11 +369,12 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       return false;
     // arrival of plane z+R: its centres enter the queue
     mbarWait(&full[sN], uint32_t(phN));
-    {
-      const V4<T> c = ld4(stages + size_t(sN) * C::SSTRIDE + rowOwn + C::PADX + x0);
+#pragma unroll
+    for (int h = 0; h < NV; ++h) {
+      const V4<T> c = ld4(stages + size_t(sN) * C::SSTRIDE + rowOwn + C::PADX + x0 + 4 * h);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        q[(U + 2 * R) % Q][j] = c.v[j];
+        q[(U + 2 * R) % Q][4 * h + j] = c.v[j];
     }
     if (++sN == NS) {
       sN = 0;
@@ -367,25 +383,29 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     // x / y neighbours of plane z from its stage
     const T *st = stages + size_t(sC) * C::SSTRIDE;
     const V4<T> L = ld4(st + rowOwn + x0);
-    const V4<T> Rr = ld4(st + rowOwn + 2 * C::PADX + x0);
-    V4<T> yp[NT], ym[NT];
+    const V4<T> Rr = ld4(st + rowOwn + C::PADX + x0 + PTS);
+    V4<T> yp[NT][NV], ym[NT][NV];
     if constexpr (RANK == 3) {
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        yp[t] = ld4(st + rowOwn + Taps<NT>::k(t) * C::CW + C::PADX + x0);
-        ym[t] = ld4(st + rowOwn - Taps<NT>::k(t) * C::CW + C::PADX + x0);
-      }
+      for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int h = 0; h < NV; ++h) {
+          yp[t][h] = ld4(st + rowOwn + Taps<NT>::k(t) * C::CW + C::PADX + x0 + 4 * h);
+          ym[t][h] = ld4(st + rowOwn - Taps<NT>::k(t) * C::CW + C::PADX + x0 + 4 * h);
+        }
     }
-    V4<T> pv;
+    V4<T> pv[NV];
     if constexpr (C::WAVE)
-      pv = ld4(pstages + size_t(sC) * C::PSTAGE + ty * C::TX + x0);
+#pragma unroll
+      for (int h = 0; h < NV; ++h)
+        pv[h] = ld4(pstages + size_t(sC) * C::PSTAGE + ty * C::TX + x0 + 4 * h);
     const int sDone = sC;
     if (++sC == NS)
       sC = 0;
 
     constexpr int cz = (U + R) % Q;
-    V4<T> o;
-    if constexpr (kPackF32<T>) {
+    T o[PTS];
+    if constexpr (kPackF32<T> && PTS == 4) {
       // points (j, j+1) as one f32x2 lane pair: the same op sequence as the scalar branch
       // below, every product fenced (see pfence)
       const uint32_t z0 = P.zero;
@@ -408,8 +428,8 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         if constexpr (RANK == 3) {
 #pragma unroll
           for (int t = 0; t < NT; ++t)
-            acc = add2(acc, pfence(mul2(add2(pk2(yp[t].v[j], yp[t].v[j + 1]),
-                                             pk2(ym[t].v[j], ym[t].v[j + 1])),
+            acc = add2(acc, pfence(mul2(add2(pk2(yp[t][0].v[j], yp[t][0].v[j + 1]),
+                                             pk2(ym[t][0].v[j], ym[t][0].v[j + 1])),
                                         P.pwy[t]),
                                    z0));
         }
@@ -423,15 +443,15 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         }
         f2 r;
         if constexpr (C::WAVE)
-          r = add2(sub2(pfence(mul2(c, P.ptwo), z0), pk2(pv.v[j], pv.v[j + 1])),
+          r = add2(sub2(pfence(mul2(c, P.ptwo), z0), pk2(pv[0].v[j], pv[0].v[j + 1])),
                    pfence(mul2(acc, P.pscale), z0));
         else
           r = add2(c, pfence(mul2(acc, P.pscale), z0));
-        upk2(r, o.v[j], o.v[j + 1]);
+        upk2(r, o[j], o[j + 1]);
       }
     } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < PTS; ++j) {
       const T c = q[cz][j];
       // lap = c*W0; then d = 0 (z), 1 (y), rank-1 (x), taps ascending: the generator's
       // op order (kernels.cpp:110-135), one IEEE op at a time
@@ -444,31 +464,35 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       if constexpr (RANK == 3) {
 #pragma unroll
         for (int t = 0; t < NT; ++t)
-          acc = add_(acc, mul_(add_(yp[t].v[j], ym[t].v[j]), P.wy[t]));
+          acc = add_(acc, mul_(add_(yp[t][j / 4].v[j % 4], ym[t][j / 4].v[j % 4]), P.wy[t]));
       }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int k = Taps<NT>::k(t);
-        const int ip = 4 + j + k, im = 4 + j - k; // window [L | centre | Rr]
-        const T xp = ip < 4 ? L.v[ip & 3] : (ip < 8 ? q[cz][ip & 3] : Rr.v[ip & 3]);
-        const T xm = im < 4 ? L.v[im & 3] : (im < 8 ? q[cz][im & 3] : Rr.v[im & 3]);
+        const int ip = 4 + j + k, im = 4 + j - k; // window [L | centre (PTS) | Rr]
+        const T xp = ip < 4 ? L.v[ip & 3]
+                            : (ip < 4 + PTS ? q[cz][ip - 4] : Rr.v[(ip - 4 - PTS) & 3]);
+        const T xm = im < 4 ? L.v[im & 3]
+                            : (im < 4 + PTS ? q[cz][im - 4] : Rr.v[(im - 4 - PTS) & 3]);
         acc = add_(acc, mul_(add_(xp, xm), P.wx[t]));
       }
       if constexpr (C::WAVE)
-        o.v[j] = add_(sub_(mul_(c, P.two), pv.v[j]), mul_(acc, P.scale));
+        o[j] = add_(sub_(mul_(c, P.two), pv[j / 4].v[j % 4]), mul_(acc, P.scale));
       else
-        o.v[j] = add_(c, mul_(acc, P.scale));
+        o[j] = add_(c, mul_(acc, P.scale));
     }
     }
     if (yok) {
       T *dst = outRow + int64_t(m) * P.plane;
-      if (xrem >= 4) {
-        st4(dst, o);
+      if (xrem >= PTS) {
+#pragma unroll
+        for (int h = 0; h < NV; ++h)
+          st4(dst + 4 * h, V4<T>{{o[4 * h], o[4 * h + 1], o[4 * h + 2], o[4 * h + 3]}});
       } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < PTS; ++j)
           if (j < xrem)
-            dst[j] = o.v[j];
+            dst[j] = o[j];
       }
     }
     // Release a stage only once the values read from it are consumed.  ptxas may schedule an
@@ -514,10 +538,11 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
           if (lo ? yo >= P.hs[d] : yo < P.ny - P.hs[d])
             continue;
         }
-        int jmask = 0xF; // x points of this thread inside the box
+        constexpr int FULL = (1 << PTS) - 1;
+        int jmask = FULL; // x points of this thread inside the box
         if (dim == XD) {
           jmask = 0;
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < PTS; ++j) {
             const int xo = xb + x0 + j;
             if (lo ? xo < P.hs[d] : xo >= P.nx - P.hs[d])
               jmask |= 1 << j;
@@ -532,10 +557,12 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         const bool vec = (P.pdelta[d] * int64_t(sizeof(T))) % 16 == 0;
         for (int m = m0; m < m1; ++m) {
           const int64_t off = int64_t(m) * P.plane;
-          if (vec && jmask == 0xF && xrem >= 4) {
-            st4(dst + off, ld4(src + off));
+          if (vec && jmask == FULL && xrem >= PTS) {
+#pragma unroll
+            for (int h = 0; h < NV; ++h)
+              st4(dst + off + 4 * h, ld4(src + off + 4 * h));
           } else {
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < PTS; ++j)
               if ((jmask >> j & 1) && j < xrem)
                 dst[off + j] = src[off + j];
           }
@@ -739,6 +766,10 @@ template <typename T, int RANK> int dispatchNT(StarLaunch &L, cudaStream_t st, i
       return launchStarT<T, RANK, 1, kHeat, 1>(L, st, b);
     if (L.geo == 1 && s.kind == kHeat && s.ntaps == 2)
       return launchStarT<T, RANK, 2, kHeat, 1>(L, st, b);
+    if (L.geo == 2 && s.kind == kHeat && s.ntaps == 1)
+      return launchStarT<T, RANK, 1, kHeat, 2>(L, st, b);
+    if (L.geo == 2 && s.kind == kHeat && s.ntaps == 2)
+      return launchStarT<T, RANK, 2, kHeat, 2>(L, st, b);
   }
   if (s.kind == kHeat) {
     if (s.ntaps == 1) return launchStarT<T, RANK, 1, kHeat>(L, st, b);
@@ -1153,7 +1184,7 @@ int makeBoxTensorMap(int dtype, const DevLayout &lay, void *base, const uint32_t
 
 int starGeoFor(const StarSpec &s, int dtype, int rank, const int64_t *ext) {
   if (const char *e = std::getenv("HG_STAR_GEO")) // A/B experiments only
-    return std::atoi(e) == 1 && rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2;
+    return rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2 ? std::atoi(e) : 0;
   // wide tiles pay on large planes (>= 768 x 768); 512^2 planes prefer the 64 x 16 tile
   return rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2 && ext[1] >= 768 &&
                  ext[2] >= 768
@@ -1169,10 +1200,11 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
   const int es = dtype == HG_F32 ? 4 : 8;
   const int R = s.radius;
   const bool f64 = dtype != HG_F32;
-  const int TX = (rank == 3 ? (geo == 1 ? StarGeom<3, 1, 1>::TXT
+  // geo 2 is geo 1's 128 x 12 tile with 8 points per thread: same boxes
+  const int TX = (rank == 3 ? (geo >= 1 ? StarGeom<3, 1, 1>::TXT
                                         : R >= 4 ? StarGeom<3, 4>::TXT : StarGeom<3, 1>::TXT)
                             : StarGeom<2, 1>::TXT) * 4;
-  const int TY = rank == 3 ? (geo == 1 ? StarGeom<3, 1, 1>::TYT
+  const int TY = rank == 3 ? (geo >= 1 ? StarGeom<3, 1, 1>::TYT
                                        : R >= 4 ? (f64 ? StarGeom<3, 4, 0, 8>::TYT
                                                        : StarGeom<3, 4>::TYT)
                                                 : StarGeom<3, 1>::TYT)
