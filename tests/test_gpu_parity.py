@@ -507,3 +507,28 @@ def test_pageable_staged_transfers(port):
     assert perm == perm_o
     for g, p in zip(got, perm_o):
         assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
+
+
+@pytest.mark.parametrize("spec", [("heat", 2, 64, 2), ("heat", 3, 40, 4), ("wave", 3, 24, 8)])
+def test_zero_steps_leave_fields_and_binding(port, spec):
+    # runSerialStencil with timesteps = 0 (serial.cpp:57-88): no step, identity binding; a
+    # later run continues from the untouched fields (resident, star and wave paths)
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    arrays = port.initial_fields(prog)
+    plan = hg.Plan(prog)
+    try:
+        plan.init_fields()
+        plan.run(0)
+        perm, steps = plan.binding()
+        assert steps == 0 and perm == list(range(prog.nfields))
+        for i, a in enumerate(arrays):
+            assert np.array_equal(plan.download(i).view(np.uint32), a.view(np.uint32))
+        plan.run(3)
+        perm, _ = plan.binding()
+        got = [plan.download(p) for p in perm]
+    finally:
+        plan.close()
+    perm_o = port.run(prog, arrays, 3)
+    assert perm == perm_o
+    for g, p in zip(got, perm_o):
+        assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
