@@ -532,3 +532,27 @@ def test_zero_steps_leave_fields_and_binding(port, spec):
     assert perm == perm_o
     for g, p in zip(got, perm_o):
         assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
+
+
+def test_live_upload_multi_apply(port):
+    # hg_plan_upload_live on a multi-apply step: the skipped box is the stencil.store region
+    # of the output field (mstore), over poisoned device buffers
+    from paper_2404_02218_b200.programs.flux3d import xir
+    prog = hg.Program.parse(xir(20, 18, 37))[0]
+    arrays = port.initial_fields(prog)
+    plan = hg.Plan(prog)
+    try:
+        for i in range(prog.nfields):
+            plan.upload(i, np.full_like(arrays[i], np.float32(1e30)))
+        import torch
+        for i, a in enumerate(arrays):
+            plan.upload(i, torch.from_numpy(a.copy()).pin_memory().numpy(), live=True)
+        plan.run(3)
+        perm, _ = plan.binding()
+        got = [plan.download(p) for p in perm]
+    finally:
+        plan.close()
+    perm_o = port.run(prog, arrays, 3)
+    assert perm == perm_o
+    for g, p in zip(got, perm_o):
+        assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))

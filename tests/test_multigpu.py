@@ -28,6 +28,11 @@ def _ngpus():
      "--calls", "1,3,5"],
     ["--kind", "heat", "--rank", "3", "--extent", "100", "--order", "8", "--T", "6",
      "--calls", "4,2"],
+    # bench.py's e2e path: pinned host fields, live uploads over poisoned buffers, then runs
+    ["--kind", "heat", "--rank", "3", "--extent", "48", "--order", "4", "--T", "5",
+     "--calls", "2,3", "--upload"],
+    ["--kind", "wave", "--rank", "3", "--extent", "40", "--order", "8", "--T", "4",
+     "--upload"],
 ])
 def test_ipc_dmp_two_ranks(args):
     n = _ngpus()

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--calls", default=None, help="split T over several run calls, e.g. 2,3")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="p2p: hg_dmp (fused NVLink puts); nccl: the packed-box NCCL baseline")
+    ap.add_argument("--upload", action="store_true",
+                    help="the e2e path of bench.py: fields from pinned host buffers via "
+                         "hg_plan_upload_live over poisoned device buffers")
     ap.add_argument("--golden", default=None,
                     help="a decomposed_authored program of tests/golden (multi-apply)")
     a = ap.parse_args()
@@ -59,6 +62,18 @@ def main():
         dmp = hg.Dmp(plan, dc, rank)
         hd.connect(dmp, rank, grid, world)
     dist.barrier()
+    if a.upload:
+        host = [torch.from_numpy(plan.download(i)).pin_memory().numpy()
+                for i in range(local.nfields)]
+        for i in range(local.nfields):  # poison: a skipped region that mattered would show
+            plan.upload(i, np.full_like(host[i], np.float32(1e30)))
+        plan.reset_binding()
+        for i in range(local.nfields):
+            plan.upload(i, host[i], live=True)
+        if a.transport != "nccl":
+            dmp.invalidate()
+        torch.cuda.synchronize()
+        dist.barrier()
     calls = [int(x) for x in a.calls.split(",")] if a.calls else [a.T]
     assert sum(calls) == a.T
     for c in calls:
