@@ -188,10 +188,15 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   const int sstride = (stage + ve - 1) / ve * ve;
   // TMA planes in flight beyond the 2RZ+1 window: 6 where shared memory allows (PW set:
   // 214 -> 224 GPts/s from depth 3 to 6, profiles/r1_sweeps.md), down to 1
-  static const int want = [] {
+  static const int envDepth = [] {
     const char *e = std::getenv("HG_JIT_DEPTH"); // tuning experiments only
-    return e ? std::max(1, std::atoi(e)) : 6;
+    return e ? std::max(1, std::atoi(e)) : 0;
   }();
+  // >= 3 operand slabs per plane: a 3-deep ring keeps two CTAs per SM (with 16-plane chunks,
+  // jitLaunch; PW set 222-224 -> 230-231 GPts/s, profiles/r1_sweeps.md); fewer operands
+  // keep the 6-deep ring
+  const int want = envDepth ? envDepth : (O >= 3 ? 3 : 6);
+  K.deep = want;
   auto smemFor = [&](int d) {
     return 128 + static_cast<size_t>(es) * (2 * rz + 1 + d) * O * sstride + 2 * (2 * rz + 1 + d) * 8;
   };
@@ -493,8 +498,10 @@ int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
   xs -= mis;
   nx += mis;
   int tiles_x = (nx + K.tx - 1) / K.tx, tiles_y = (ny + K.ty - 1) / K.ty;
-  // z-chunks of ~32 planes (measured best for the PW set: 4 chunks at nz=128)
-  int nch = chunks > 0 ? chunks : std::max(1, (nz + 16) / 32);
+  // z-chunks of ~32 planes; ~16 with the 3-deep ring of multi-operand programs (two CTAs per
+  // SM: more, shorter units balance the waves)
+  const int zc = K.deep <= 3 ? 16 : 32;
+  int nch = chunks > 0 ? chunks : std::max(1, (nz + zc / 2) / zc);
   int chunk = (nz + nch - 1) / nch;
   nch = (nz + chunk - 1) / chunk;
   int iv[10] = {zs, ys, xs, nz, ny, nx, tiles_x, tiles_y, chunk, nch};
