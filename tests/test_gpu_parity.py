@@ -415,20 +415,25 @@ def test_shallow_tma_ring_reuse_bitwise(fuse):
 
 
 @pytest.mark.parametrize("pinned", [True, False])
-@pytest.mark.parametrize("spec,T", [(("heat", 3, 67, 4), 3), (("wave", 3, 45, 8), 4),
-                                    (("heat", 2, 301, 2), 5), (("heat", 3, 40, 2), 1)])
-def test_host_transfers_and_live_upload(port, pinned, spec, T):
+@pytest.mark.parametrize("spec,T,dtype", [
+    (("heat", 3, 67, 4), 3, "f32"), (("wave", 3, 45, 8), 4, "f32"),
+    (("heat", 2, 301, 2), 5, "f32"), (("heat", 3, 40, 2), 1, "f32"),
+    (("heat", 3, 37, 4), 2, "f64"), (("heat", 2, 1023, 2), 4, "f32"),
+    (("heat", 2, 203, 4), 3, "f64")])
+def test_host_transfers_and_live_upload(port, pinned, spec, T, dtype):
     # uploads/downloads from pinned host memory (zero-copy kernel) and pageable memory (copy
     # engines); the live upload leaves the output slot's store box unmoved -- garbage there
-    # must not matter, since step 1 overwrites it before anything reads it
+    # must not matter, since step 1 overwrites it before anything reads it (2D heat cases
+    # run through the resident whole-run kernel)
     import torch
-    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    prog = hg.build_kernel(hg.KernelSpec(*spec, dtype))
+    u = np.uint32 if dtype == "f32" else np.uint64
     arrays = port.initial_fields(prog)
     plan = hg.Plan(prog)
     try:
         # poison every buffer first, so a skipped region that mattered would show
         for i in range(prog.nfields):
-            plan.upload(i, np.full_like(arrays[i], np.float32(1e30)))
+            plan.upload(i, np.full_like(arrays[i], 1e30))
         hosts = []
         for i, a in enumerate(arrays):
             h = torch.from_numpy(a.copy()).pin_memory().numpy() if pinned else a.copy()
@@ -436,7 +441,7 @@ def test_host_transfers_and_live_upload(port, pinned, spec, T):
             plan.upload(i, h, live=True)
         # a full upload of buffer 0 round-trips exactly
         back = plan.download(0)
-        assert np.array_equal(back.view(np.uint32), arrays[0].view(np.uint32))
+        assert np.array_equal(back.view(u), arrays[0].view(u))
         plan.run(T)
         perm, _ = plan.binding()
         outs = []
@@ -450,7 +455,7 @@ def test_host_transfers_and_live_upload(port, pinned, spec, T):
     perm_o = port.run(prog, arrays, T)
     assert perm == perm_o
     for g, p in zip(outs, perm_o):
-        assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
+        assert np.array_equal(g.view(u), arrays[p].view(u))
 
 
 @pytest.mark.parametrize("spec,T", [
