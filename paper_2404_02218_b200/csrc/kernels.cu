@@ -118,6 +118,11 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
 #ifndef HG_MINB_G2
 #define HG_MINB_G2 3
 #endif
+// planes per TMA ring slot (1 or 2): with 2, one box of two planes lands on one mbarrier, so
+// consumers wait, and release, once per two planes (A/B: HG_ZP=2)
+#ifndef HG_ZP
+#define HG_ZP 1
+#endif
 // L2 eviction hints on the z-halo planes shared by consecutive chunks (A/B: HG_L2HINT=0)
 #ifndef HG_L2HINT
 #define HG_L2HINT 1
@@ -177,11 +182,13 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
                    : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
   static constexpr int DEPTH =
       RANK == 3 ? (R <= 2 ? HG_DEPTH3 : (sizeof(T) == 8 ? 5 : HG_DEPTH3W)) : HG_DEPTH2;
-  static constexpr int NS = R + 1 + DEPTH;
+  static constexpr int ZP = HG_ZP;                  // planes per ring slot
+  static constexpr int NS = (R + 1 + DEPTH + ZP - 1) / ZP; // ring slots
   static constexpr int Q = 2 * R + 1;
-  static constexpr int STAGE = ROWS * CW;   // elements
-  static constexpr int SSTRIDE = (STAGE + int(128 / sizeof(T)) - 1) / int(128 / sizeof(T)) * int(128 / sizeof(T));
-  static constexpr int PSTAGE = TY * TX;    // elements (wave prev)
+  static constexpr int STAGE = ROWS * CW;   // elements of one plane
+  // one slot: ZP planes back to back (the TMA box layout), 128-byte aligned
+  static constexpr int SSTRIDE = (ZP * STAGE + int(128 / sizeof(T)) - 1) / int(128 / sizeof(T)) * int(128 / sizeof(T));
+  static constexpr int PSTAGE = ZP * TY * TX;    // elements (wave prev) per slot
   static constexpr bool WAVE = KIND == kWave;
   static constexpr size_t SMEM =
       128 + sizeof(T) * (size_t(NS) * SSTRIDE + (WAVE ? size_t(NS) * PSTAGE : 0)) +
@@ -279,7 +286,8 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       const int cx = int(P.col0) + P.xs + xb - C::PADX;
       const int cy = RANK == 3 ? P.ys + yb - RY : 0;
       const int z0 = P.zs + zb - R;
-      constexpr uint32_t curBytes = uint32_t(C::STAGE * sizeof(T));
+      constexpr int ZP = C::ZP;
+      constexpr uint32_t curBytes = uint32_t(ZP * C::STAGE * sizeof(T));
       constexpr uint32_t prevBytes = uint32_t(C::PSTAGE * sizeof(T));
       // z-halo planes shared with the neighbouring chunks of this column: the last 2R planes
       // this chunk loads are the first 2R of the next chunk -- keep them in L2 (evict_last)
@@ -289,13 +297,16 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       const bool hintL2 = HG_L2HINT && !C::WAVE && P.nchunks > 1;
       const uint64_t keep = hintL2 ? l2PolicyEvictLast() : 0;
       const uint64_t drop = hintL2 ? l2PolicyEvictFirst() : 0;
-      for (int i = 0; i < n + 2 * R; ++i) {
-        const int s = i % NS;
-        if (i >= NS)
-          mbarWait(&empty[s], uint32_t((i / NS - 1) & 1));
-        const bool wantPrev = C::WAVE && i >= R && i < n + R;
+      // slot p holds planes p*ZP .. p*ZP+ZP-1 (plane i is z = z0 + i); a plane past the
+      // field's end is zero-filled by TMA and never read
+      const int nslots = (n + 2 * R + ZP - 1) / ZP;
+      for (int p = 0; p < nslots; ++p) {
+        const int s = p % NS, i = p * ZP;
+        if (p >= NS)
+          mbarWait(&empty[s], uint32_t((p / NS - 1) & 1));
+        const bool wantPrev = C::WAVE && i + ZP - 1 >= R && i < n + R;
         mbarExpectTx(&full[s], curBytes + (wantPrev ? prevBytes : 0u));
-        if (hintL2 && i >= n && zb + n < P.nz)
+        if (hintL2 && i + ZP - 1 >= n && zb + n < P.nz)
           tmaLoad3dHint(stages + size_t(s) * C::SSTRIDE, &tmCur, &full[s], cx, cy, z0 + i, keep);
         else if (hintL2 && i < 2 * R && zb > 0)
           tmaLoad3dHint(stages + size_t(s) * C::SSTRIDE, &tmCur, &full[s], cx, cy, z0 + i, drop);
@@ -323,14 +334,17 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       mbarArrive(&empty[s]);
   };
 
+  constexpr int ZP = C::ZP;
   // prologue: planes 0 .. 2R-1 (z = zb-R .. zb+R-1): centres into the queue
 #pragma unroll
   for (int i = 0; i < 2 * R; ++i) {
-    const int s = i % NS;
-    mbarWait(&full[s], uint32_t((i / NS) & 1));
+    const int s = (i / ZP) % NS;
+    if (i % ZP == 0)
+      mbarWait(&full[s], uint32_t((i / ZP / NS) & 1));
 #pragma unroll
     for (int h = 0; h < NV; ++h) {
-      V4<T> c = ld4(stages + size_t(s) * C::SSTRIDE + rowOwn + C::PADX + x0 + 4 * h);
+      V4<T> c = ld4(stages + size_t(s) * C::SSTRIDE + (i % ZP) * C::STAGE + rowOwn + C::PADX +
+                    x0 + 4 * h);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         q[i][4 * h + j] = c.v[j];
@@ -358,8 +372,9 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       blockTouch |= 2 << (2 * XD);
   }
 
-  int sN = (2 * R) % NS, phN = ((2 * R) / NS) & 1; // stage/parity of the plane arriving
-  int sC = R % NS;                                  // stage of the plane being computed
+  // slot/sub-plane/parity of the plane arriving, slot/sub-plane of the plane being computed
+  int sN = ((2 * R) / ZP) % NS, zN = (2 * R) % ZP, phN = ((2 * R) / ZP / NS) & 1;
+  int sC = (R / ZP) % NS, zC = R % ZP;
 
   // One output plane; U is the position inside the Q-periodic register queue, a compile-time
   // constant so every queue index below is a register name.  Returns false past the chunk end.
@@ -367,21 +382,26 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     constexpr int U = decltype(uc)::value;
     if (m >= n)
       return false;
-    // arrival of plane z+R: its centres enter the queue
-    mbarWait(&full[sN], uint32_t(phN));
+    // arrival of plane z+R: its centres enter the queue (one wait per slot)
+    if (ZP == 1 || zN == 0)
+      mbarWait(&full[sN], uint32_t(phN));
 #pragma unroll
     for (int h = 0; h < NV; ++h) {
-      const V4<T> c = ld4(stages + size_t(sN) * C::SSTRIDE + rowOwn + C::PADX + x0 + 4 * h);
+      const V4<T> c = ld4(stages + size_t(sN) * C::SSTRIDE + zN * C::STAGE + rowOwn + C::PADX +
+                          x0 + 4 * h);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         q[(U + 2 * R) % Q][4 * h + j] = c.v[j];
     }
-    if (++sN == NS) {
-      sN = 0;
-      phN ^= 1;
+    if (++zN == ZP) {
+      zN = 0;
+      if (++sN == NS) {
+        sN = 0;
+        phN ^= 1;
+      }
     }
     // x / y neighbours of plane z from its stage
-    const T *st = stages + size_t(sC) * C::SSTRIDE;
+    const T *st = stages + size_t(sC) * C::SSTRIDE + zC * C::STAGE;
     const V4<T> L = ld4(st + rowOwn + x0);
     const V4<T> Rr = ld4(st + rowOwn + C::PADX + x0 + PTS);
     V4<T> yp[NT][NV], ym[NT][NV];
@@ -398,10 +418,15 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     if constexpr (C::WAVE)
 #pragma unroll
       for (int h = 0; h < NV; ++h)
-        pv[h] = ld4(pstages + size_t(sC) * C::PSTAGE + ty * C::TX + x0 + 4 * h);
-    const int sDone = sC;
-    if (++sC == NS)
-      sC = 0;
+        pv[h] = ld4(pstages + size_t(sC) * C::PSTAGE + zC * (C::TY * C::TX) + ty * C::TX + x0 +
+                    4 * h);
+    // the slot is done once its last plane was the computed plane
+    const int sDone = (ZP == 1 || zC == ZP - 1) ? sC : -1;
+    if (++zC == ZP) {
+      zC = 0;
+      if (++sC == NS)
+        sC = 0;
+    }
 
     constexpr int cz = (U + R) % Q;
     T o[PTS];
@@ -501,10 +526,11 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     // the stage first: the arrive follows the output stores, whose operands depend on every
     // value loaded from the stage.  A warp with no store (rows past the domain) uses none of
     // them.  Planes 0..R-1 fed only the queue and go with the first output plane.
-    release(sDone);
-    if (m == 0) {
+    if (sDone >= 0)
+      release(sDone);
+    if (m == 0) { // slots holding only planes 0..R-1 (never a computed plane)
 #pragma unroll
-      for (int i = 0; i < R; ++i)
+      for (int i = 0; i < R / ZP; ++i)
         release(i % NS);
     }
     return true;
@@ -1226,7 +1252,7 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
   cuuint32_t estr[3] = {1, 1, 1};
   const CUtensorMapDataType dt =
       dtype == HG_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-  cuuint32_t boxCur[3] = {cuuint32_t(TX + 8), cuuint32_t(TY + 2 * RY), 1};
+  cuuint32_t boxCur[3] = {cuuint32_t(TX + 8), cuuint32_t(TY + 2 * RY), cuuint32_t(HG_ZP)};
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   if (const char *e = std::getenv("HG_L2PROMO")) // tuning experiments only
     promo = e[0] == '0' ? CU_TENSOR_MAP_L2_PROMOTION_NONE
@@ -1237,7 +1263,7 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
                       CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return setError(HG_ECUDA, "cuTensorMapEncodeTiled(cur) failed: " + std::to_string(int(r)));
-  cuuint32_t boxPrev[3] = {cuuint32_t(TX), cuuint32_t(TY), 1};
+  cuuint32_t boxPrev[3] = {cuuint32_t(TX), cuuint32_t(TY), cuuint32_t(HG_ZP)};
   r = encode(prev, dt, 3, base, dims, strides, boxPrev, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
