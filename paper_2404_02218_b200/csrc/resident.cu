@@ -1,7 +1,7 @@
 // resident.cu -- whole-run 2D heat stencil with the fields resident in shared memory.
 //
 // BASELINE config 1 (heat 2D SDO2, 1024^2 f32, 100 steps) moves 8 MB per step: the per-step
-// star kernel is launch/latency-bound there (3.6 us per step with CUDA-graph replay, most of
+// star kernel is launch/latency-bound there (3.6-3.9 us per step with CUDA-graph replay, most of
 // it launch and pipeline fill).  On B200 the two ping-pong fields fit in the 148 SMs' shared
 // memory (2 x 4.2 MB against 148 x 227 KB), so one persistent launch runs ALL T steps:
 //
