@@ -362,8 +362,15 @@ def run_ours(args):
     plan = hg.Plan(local, local_rank)
     plan.init_fields(origin=origin, stream=sh)
     dmp = nccl = None
+    transport = args.transport
+    if transport == "auto":
+        # fused NVLink puts unless the grid splits the last (contiguous) dim: an x face is R
+        # columns per row, which the fused put can only store 8 bytes at a time, so packed
+        # boxes over NCCL win there (strong 2048^3, 4 GPUs: 1x1x4 2145 vs 1054 GPts/s,
+        # 1x2x2 2428 vs 2301; 2x2x1 2458 vs 2651 -- DESIGN.md section 5)
+        transport = "nccl" if grid[-1] > 1 else "p2p"
     if world > 1 and dc is not None:
-        if args.transport == "nccl":   # the comparison baseline, not the product path
+        if transport == "nccl":   # packed boxes over NCCL send/recv
             nccl = hd.NcclSwap(plan, dc, rank, grid, stream=sh)
         else:
             dmp = hg.Dmp(plan, dc, rank)
@@ -512,8 +519,8 @@ def run_ours(args):
                               if args.workload == "heat2d_1024" else
                               f"inputs >> 126 MB L2 ({plan_bytes(local) / 1e9:.1f} GB of fields "
                               f"per GPU), no flush needed"),
-                       "transport": ("NCCL send/recv of packed boxes (baseline)"
-                                     if args.transport == "nccl" else
+                       "transport": ("NCCL send/recv of packed boxes"
+                                     if transport == "nccl" else
                                      "NVLink P2P put (CUDA IPC) + system-scope flags")
                        if world > 1 else "none"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -545,9 +552,10 @@ def main():
     ap.add_argument("--grid", default=None, help="process grid AxBxC (default: weak N x 1 x 1, "
                                                  "strong 1/2x1x1/2x2x1/2x2x2)")
     ap.add_argument("--mode", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="halo transport at N>1: p2p = the product (fused NVLink puts), "
-                         "nccl = packed boxes over NCCL send/recv (comparison baseline)")
+    ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="halo transport at N>1: p2p = fused NVLink puts from the stencil "
+                         "kernel, nccl = packed boxes over NCCL send/recv, auto = p2p unless "
+                         "the grid splits the last dim")
     ap.add_argument("--workload", default="heat3d_weak", choices=list(WORKLOADS))
     ap.add_argument("--strong-extent", type=int, default=2048)
     ap.add_argument("--e2e-timesteps", type=int, default=100)
