@@ -131,3 +131,33 @@ def test_simulate_ranks_spread_over_devices(port, spec, grid, T):
     perm = port.run(prog, arrays, T)
     for b, p in zip(out, perm):
         assert np.array_equal(b.data.view(np.uint32), arrays[p].view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,order,extents,grid,T,calls", [
+    # heat SDO4, local 256x64x64 per rank: 4 z-chunks -> boundary_last reorder + per-chunk
+    # fused-put completion counters on the z faces
+    ("heat", 4, "512x64x64", "2x1x1", 5, "2,3"),
+    ("heat", 4, "512x128x64", "2x2x1", 4, None),
+    # wave SDO8, local 400x48x48: 3 chunks, radius 4, the 3-cycle rotation
+    ("wave", 8, "800x48x48", "2x1x1", 4, "1,3"),
+    # the wide 128x12 tile (planes >= 768^2) with 3 chunks per rank: the bench's kernel
+    ("heat", 4, "400x800x800", "2x1x1", 3, None),
+    ("heat", 4, "400x800x800", "4x1x1", 3, None),
+    ("heat", 4, "512x256x128", "1x2x2", 3, None),
+])
+def test_ipc_dmp_multi_chunk(kind, order, extents, grid, T, calls):
+    # the per-rank shapes of the weak/strong bench (many z-chunks per
+    # rank) under the oracle's restatement of RankHooks::swap, halos included
+    n = _ngpus()
+    nproc = int(np.prod([int(x) for x in grid.split("x")]))
+    if n < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node",
+           str(nproc), os.path.join(REPO, "tools", "dmp_check.py"), "--kind", kind, "--rank",
+           "3", "--order", str(order), "--extents", extents, "--grid", grid, "--T", str(T)]
+    if calls:
+        cmd += ["--calls", calls]
+    r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout

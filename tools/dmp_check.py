@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--extent", type=int, default=48)
     ap.add_argument("--order", type=int, default=4)
     ap.add_argument("--grid", default=None)
+    ap.add_argument("--extents", default=None,
+                    help="global core extents AxBxC (non-cubic; overrides --extent)")
     ap.add_argument("--T", type=int, default=5)
     ap.add_argument("--calls", default=None, help="split T over several run calls, e.g. 2,3")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -51,6 +53,8 @@ def main():
         grid = [int(x) for x in a.grid.split("x")] if a.grid else case["grid"]
     else:
         prog = hg.build_kernel(hg.KernelSpec(a.kind, a.rank, a.extent, a.order, "f32"))
+        if a.extents:
+            prog = prog.with_extents([int(x) for x in a.extents.split("x")])
     local, dc = prog.decompose(grid)
     plan = hg.Plan(local, lr)
     coord = hg.coord_from_rank(rank, grid)
