@@ -361,26 +361,18 @@ def run_ours(args):
         local, dc, origin = wl["build"](hg), None, None
     plan = hg.Plan(local, local_rank)
     plan.init_fields(origin=origin, stream=sh)
-    dmp = nccl = None
+    dmp = None
     transport = args.transport
     if transport == "auto":
-        # fused NVLink puts unless the grid splits the last (contiguous) dim: an x face is R
-        # columns per row, which the fused put can only store 8 bytes at a time, so packed
-        # boxes over NCCL win there (strong 2048^3, 4 GPUs: 1x1x4 2145 vs 1054 GPts/s,
-        # 1x2x2 2428 vs 2301; 2x2x1 2458 vs 2651 -- DESIGN.md section 5)
-        transport = "nccl" if grid[-1] > 1 else "p2p"
+        # the fused NVLink path for every grid: x faces (the contiguous last dim) travel as
+        # packed slabs there, so no grid needs the NCCL transport
+        transport = "p2p"
     if world > 1 and dc is not None:
-        if transport == "nccl":   # packed boxes over NCCL send/recv
-            nccl = hd.NcclSwap(plan, dc, rank, grid, stream=sh)
-        else:
-            dmp = hg.Dmp(plan, dc, rank)
-            hd.connect(dmp, rank, grid, world)
+        dmp = hd.make_dmp(plan, dc, rank, grid, world, transport=transport)
         dist.barrier()
 
     def steps(k):
-        if nccl is not None:
-            nccl.run(k)
-        elif dmp is None:
+        if dmp is None:
             plan.run(k, stream=sh)
         else:
             dmp.run(k, stream=sh)
@@ -471,6 +463,8 @@ def run_ours(args):
             for i in range(local.nfields):
                 plan.upload(i, host[i].numpy(), stream=sh, live=True)
             if dmp is not None:
+                # collective: the next run first performs the receiver-ready handshake (no
+                # neighbour puts into a buffer whose upload is still in flight)
                 dmp.invalidate()
             steps(T)
             perm, _ = plan.binding()
@@ -491,8 +485,9 @@ def run_ours(args):
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
         secs = float(el.item())
         e2e = {"value": core_local * world * T * n_calls / secs / 1e9, "unit": "GPts/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "step": f"one runSerialStencil-style call: upload fields from pinned host "
+               "h2d_bytes_per_step": h2d // T, "d2h_bytes_per_step": d2h // T,
+               "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h, "timesteps_per_call": T,
+               "call": f"one runSerialStencil-style call: upload fields from pinned host "
                        f"(zero-copy kernel; the output slot's core, overwritten unread by "
                        f"step 1, is not moved), {T} time steps, download the final binding "
                        f"(per rank)",
@@ -519,9 +514,11 @@ def run_ours(args):
                               if args.workload == "heat2d_1024" else
                               f"inputs >> 126 MB L2 ({plan_bytes(local) / 1e9:.1f} GB of fields "
                               f"per GPU), no flush needed"),
-                       "transport": ("NCCL send/recv of packed boxes"
+                       "transport": ("NCCL send/recv of packed boxes (C++, side stream, "
+                                     "overlapped with the interior units)"
                                      if transport == "nccl" else
-                                     "NVLink P2P put (CUDA IPC) + system-scope flags")
+                                     "NVLink P2P stores fused into the stencil kernel (CUDA "
+                                     "IPC) + system-scope flags; x faces as packed slabs")
                        if world > 1 else "none"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -553,9 +550,9 @@ def main():
                                                  "strong 1/2x1x1/2x2x1/2x2x2)")
     ap.add_argument("--mode", default="weak", choices=["weak", "strong"])
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
-                    help="halo transport at N>1: p2p = fused NVLink puts from the stencil "
-                         "kernel, nccl = packed boxes over NCCL send/recv, auto = p2p unless "
-                         "the grid splits the last dim")
+                    help="halo transport at N>1: p2p = fused NVLink stores from the stencil "
+                         "kernel, nccl = packed boxes over NCCL send/recv on a side stream "
+                         "(C++), auto = p2p")
     ap.add_argument("--workload", default="heat3d_weak", choices=list(WORKLOADS))
     ap.add_argument("--strong-extent", type=int, default=2048)
     ap.add_argument("--e2e-timesteps", type=int, default=100)

@@ -274,22 +274,50 @@ int hg_plan_synchronize(hg_plan *plan);
 /* Kernel launches issued by this plan so far (for bench/gpu_launches accounting). */
 int64_t hg_plan_launch_count(const hg_plan *plan);
 
-/* ---- dmp: halo swap across ranks over NVLink peer memory -------------------------------- */
+/* ---- dmp: halo swap across ranks (NVLink peer memory or NCCL) -------------------------- */
+#define HG_TRANSPORT_P2P 0  /* NVLink peer stores fused into the stencil kernel + flags */
+#define HG_TRANSPORT_NCCL 1 /* packed boxes, NCCL send/recv on a side stream, overlapped */
+#define HG_NCCL_ID_BYTES 128
+typedef struct hg_dmp_opts {
+  int transport;                            /* HG_TRANSPORT_P2P (default) | _NCCL */
+  int nranks;                               /* NCCL: ranks in the communicator (= grid size) */
+  unsigned char nccl_id[HG_NCCL_ID_BYTES];  /* NCCL: hg_nccl_unique_id() of one rank, shared */
+  double timeout_s;                         /* bounded halo waits: 0 = default (30 s),
+                                               < 0 = wait forever */
+} hg_dmp_opts;
+/* One rank's endpoint of the decomposed program (RankHooks + Endpoint, simulator.cpp:201-260,
+ * 772-834).  hg_dmp_create = hg_dmp_create_ex with default options (P2P). */
 int hg_dmp_create(hg_plan *plan, const hg_decomp *decomp, int64_t rank, hg_dmp **out);
+/* NCCL: every rank calls this concurrently (ncclCommInitRank) with the same id. */
+int hg_dmp_create_ex(hg_plan *plan, const hg_decomp *decomp, int64_t rank,
+                     const hg_dmp_opts *opts, hg_dmp **out);
+int hg_nccl_unique_id(void *id /* HG_NCCL_ID_BYTES */);
 int hg_dmp_destroy(hg_dmp *dmp);
-/* Multi-process: export this rank's CUDA IPC handles (buffers + signal flags) as a blob,
- * all-gather the blobs with any host transport, import every neighbour's. */
+/* P2P multi-process: export this rank's CUDA IPC handles (buffers, packed x-face receive
+ * slabs, signal flags) as a blob, all-gather the blobs with any host transport, import every
+ * neighbour's. */
 int hg_dmp_ipc_export(hg_dmp *dmp, void *blob, size_t cap, size_t *len);
 int hg_dmp_ipc_import(hg_dmp *dmp, int64_t peer_rank, const void *blob, size_t len);
-/* Time steps of this rank: swap dirty fields (direct NVLink puts into the neighbours' halos +
- * a release flag), wait for the neighbours' flags, compute.  Collective over all ranks. */
+/* Time steps of this rank: swap dirty fields, wait for the neighbours' halos, compute.
+ * Collective over all ranks (every rank runs the same step counts).  Asynchronous on
+ * `stream`.  A halo wait that exceeds the timeout (a stuck or dead peer) does not hang the
+ * GPU: it is recorded, hg_dmp_status reports it, and later calls return HG_ETRAP. */
 int hg_dmp_run(hg_dmp *dmp, int64_t steps, void *stream);
-/* Single process: connect the n ranks (peer pointers) and run all of them step by step,
- * ordering swap and compute phases with CUDA events (simulate's loop). */
+/* Waits for the dmp's queued work; HG_ETRAP ("rank r: halo round from neighbour rank n
+ * (face ...) did not arrive for epoch e within X s") if a halo wait timed out. */
+int hg_dmp_status(hg_dmp *dmp);
+int hg_dmp_set_timeout(hg_dmp *dmp, double seconds /* <= 0: forever */);
+/* Single process: connect the n ranks (peer pointers).  hg_sim_run runs all of them step by
+ * step: with one rank per device, the multi-process protocol (fused NVLink swap, in-kernel
+ * waits); ranks sharing a device are ordered by CUDA events (simulate's loop,
+ * simulator.cpp:1066-1203).  Returns after the ranks finished (HG_ETRAP on a timed-out wait). */
 int hg_sim_connect(hg_dmp **ranks, int n);
 int hg_sim_run(hg_dmp **ranks, int n, int64_t steps, void **streams);
 int64_t hg_dmp_bytes_exchanged(const hg_dmp *dmp); /* payload bytes put so far */
-/* Host data was uploaded into the plan's buffers: every halo is stale, swap all on next use. */
+/* Host data was uploaded into the plan's buffers: every halo is stale, swap all on next use.
+ * Collective in multi-process P2P mode: every rank calls it after its own uploads (on the
+ * stream of its next hg_dmp_run, or fenced before it); the next run first performs a
+ * receiver-ready handshake so no neighbour puts into a buffer still being uploaded. */
 int hg_dmp_invalidate(hg_dmp *dmp);
 
 #ifdef __cplusplus

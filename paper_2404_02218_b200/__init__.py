@@ -14,7 +14,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _capi as capi
-from ._capi import HgDecomp, HgExchange, HgLayout, HgOp, HgProgram, check, lib
+from ._capi import HgDecomp, HgError, HgExchange, HgLayout, HgOp, HgProgram, check, lib  # noqa: F401
 
 __all__ = [
     "KernelSpec", "Program", "Buffer", "Plan", "Dmp", "build_kernel", "initial_fields",
@@ -454,14 +454,28 @@ def run_serial_stencil(prog: Program, fields: List[Buffer], timesteps: int,
 
 # ---- dmp -------------------------------------------------------------------------------------
 class Dmp:
-    """One rank's halo-swap endpoint (hg_dmp) over a local plan."""
+    """One rank's halo-swap endpoint (hg_dmp) over a local plan.
 
-    def __init__(self, plan: Plan, decomp: HgDecomp, rank: int):
+    transport "p2p" (default): NVLink peer stores fused into the stencil kernel (connect the
+    ranks with export()/import_peer(), see dist.connect).  transport "nccl": packed boxes over
+    NCCL send/recv on a side stream; every rank passes the same `nccl_id` (nccl_unique_id() on
+    one rank, shared by the host) and `nranks`.  timeout_s bounds every halo wait (0: the
+    library default, < 0: forever)."""
+
+    def __init__(self, plan: Plan, decomp: HgDecomp, rank: int, transport: str = "p2p",
+                 nccl_id: Optional[bytes] = None, nranks: int = 0, timeout_s: float = 0.0):
         self.plan = plan
         h = C.c_void_p()
-        check(lib().hg_dmp_create(plan.h, C.byref(decomp), rank, C.byref(h)))
+        o = capi.HgDmpOpts()
+        o.transport = capi.HG_TRANSPORT_NCCL if transport == "nccl" else capi.HG_TRANSPORT_P2P
+        o.nranks = nranks
+        o.timeout_s = timeout_s
+        if nccl_id is not None:
+            C.memmove(o.nccl_id, nccl_id, capi.HG_NCCL_ID_BYTES)
+        check(lib().hg_dmp_create_ex(plan.h, C.byref(decomp), rank, C.byref(o), C.byref(h)))
         self.h = h
         self.rank = rank
+        self.transport = transport
 
     def close(self):
         if self.h:
@@ -482,12 +496,26 @@ class Dmp:
     def run(self, steps: int, stream=None):
         check(lib().hg_dmp_run(self.h, steps, stream))
 
+    def status(self):
+        """Wait for the queued work; raises HgError(HG_ETRAP) if a halo wait timed out."""
+        check(lib().hg_dmp_status(self.h))
+
+    def set_timeout(self, seconds: float):
+        check(lib().hg_dmp_set_timeout(self.h, seconds))
+
     def bytes_exchanged(self) -> int:
         return int(lib().hg_dmp_bytes_exchanged(self.h))
 
     def invalidate(self):
-        """Host data was uploaded: every halo is stale."""
+        """Host data was uploaded: every halo is stale (collective across P2P ranks)."""
         check(lib().hg_dmp_invalidate(self.h))
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (for Dmp(..., transport="nccl"))."""
+    buf = C.create_string_buffer(capi.HG_NCCL_ID_BYTES)
+    check(lib().hg_nccl_unique_id(buf))
+    return buf.raw
 
 
 def simulate(prog: Program, grid: Sequence[int], global_init: List[Buffer], timesteps: int,

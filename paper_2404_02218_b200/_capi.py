@@ -19,6 +19,8 @@ HG_MAX_STORES = 16
 
 HG_OK, HG_EINVAL, HG_EUNSUPPORTED, HG_ECUDA, HG_ETRAP, HG_ENOMEM, HG_ESTATE = range(7)
 HG_F32, HG_F64 = 1, 2
+HG_TRANSPORT_P2P, HG_TRANSPORT_NCCL = 0, 1
+HG_NCCL_ID_BYTES = 128
 HG_OP_ACCESS, HG_OP_CONST, HG_OP_ADD, HG_OP_SUB, HG_OP_MUL, HG_OP_DIV = 1, 2, 3, 4, 5, 6
 
 i64x3 = C.c_int64 * HG_MAX_RANK
@@ -27,6 +29,11 @@ i64x3 = C.c_int64 * HG_MAX_RANK
 class HgOp(C.Structure):
     _fields_ = [("code", C.c_int32), ("a", C.c_int32), ("b", C.c_int32),
                 ("operand", C.c_int32), ("off", i64x3), ("bits", C.c_uint64)]
+
+
+class HgDmpOpts(C.Structure):
+    _fields_ = [("transport", C.c_int), ("nranks", C.c_int),
+                ("nccl_id", C.c_ubyte * HG_NCCL_ID_BYTES), ("timeout_s", C.c_double)]
 
 
 class HgBounds(C.Structure):
@@ -137,6 +144,10 @@ def lib() -> C.CDLL:
         "hg_plan_synchronize": (C.c_int, [V]),
         "hg_plan_set_tuning": (C.c_int, [V, C.c_int, C.c_int]),
         "hg_dmp_create": (C.c_int, [V, P(HgDecomp), I64, P(V)]),
+        "hg_dmp_create_ex": (C.c_int, [V, P(HgDecomp), I64, P(HgDmpOpts), P(V)]),
+        "hg_nccl_unique_id": (C.c_int, [V]),
+        "hg_dmp_status": (C.c_int, [V]),
+        "hg_dmp_set_timeout": (C.c_int, [V, C.c_double]),
         "hg_dmp_destroy": (C.c_int, [V]),
         "hg_dmp_ipc_export": (C.c_int, [V, V, SZ, P(SZ)]),
         "hg_dmp_ipc_import": (C.c_int, [V, I64, V, SZ]),

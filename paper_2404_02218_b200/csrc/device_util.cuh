@@ -134,6 +134,42 @@ __device__ __forceinline__ void tmaLoad3dHint(void *dst, const CUtensorMap *map,
                : "memory");
 }
 
+// ---- bounded flag waits (stuck-peer detection) -----------------------------------------------
+__device__ __forceinline__ uint64_t globalNs() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spins until *flag >= epoch (system-scope acquire: the peer's release store and every byte it
+// wrote before it are visible).  With timeout_ns > 0 it gives up after that long, records
+// `code` in *err (first error wins) and returns false; it also gives up at once when another
+// waiter already recorded an error, so a dead peer costs one timeout, not one per waiter.
+// The reference reports a deadlock instead of hanging (simulator.cpp:143-173, 1174-1187).
+__device__ __forceinline__ bool waitFlag(const unsigned long long *flag, unsigned long long epoch,
+                                         unsigned long long *err, unsigned long long timeout_ns,
+                                         unsigned long long code) {
+  unsigned long long v;
+  uint64_t t0 = 0;
+  for (unsigned spin = 0;; ++spin) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= epoch)
+      return true;
+    if (timeout_ns && (spin & 63) == 0) {
+      const uint64_t now = globalNs();
+      if (t0 == 0)
+        t0 = now;
+      unsigned long long e = 0;
+      if (err)
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(e) : "l"(err) : "memory");
+      if (e != 0 || now - t0 > timeout_ns) {
+        if (err && e == 0)
+          atomicCAS(err, 0ull, code);
+        return false;
+      }
+    }
+  }
+}
+
 // Calls f(mb + U, integral_constant<U>) for U = 0, 1, ... while it returns true.
 template <typename F, int... Us>
 __device__ __forceinline__ void unrolled(F &f, int mb, std::integer_sequence<int, Us...>) {

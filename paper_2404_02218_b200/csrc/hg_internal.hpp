@@ -40,8 +40,22 @@ struct Analysis {
   int period = 1;              // lcm of group lengths
 };
 
-// Validates + classifies.  Returns HG_OK or an error status (message set).
-int analyze(const hg_program &p, Analysis &out);
+// Validates + classifies.  Returns HG_OK or an error status (message set).  allowStar = false
+// sends star programs to the fused-apply family (HG_NO_STAR, tests).
+int analyze(const hg_program &p, Analysis &out, bool allowStar = true);
+
+// ---- family selectors (tests and A/B runs) ---------------------------------------------
+// Read from the environment ONCE per plan, in hg_plan_create; no launcher reads it.
+struct Knobs {
+  bool noStar = false;        // HG_NO_STAR=1: star programs through the fused-apply family
+  bool noApplyJit = false;    // HG_NO_APPLY_JIT=1: the generic kernel, not generated code
+  bool noFuseApplies = false; // HG_NO_FUSE_APPLIES=1: multi-apply steps apply by apply
+  bool noResident = false;    // HG_NO_RESIDENT=1: 2D heat step by step
+  bool tb = false;            // HG_TB=1: two-step passes for large 3D heat (opt-in)
+  int starGeo = -1;           // HG_STAR_GEO=n: force the star tile geometry
+  int jitDepth = 0;           // HG_JIT_DEPTH=n: TMA ring depth of the fused-apply family
+};
+Knobs readKnobs();
 int validateProgram(const hg_program &p);
 
 // the stores of either program form (single apply: one per result; multi-apply: nstores)

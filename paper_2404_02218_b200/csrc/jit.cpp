@@ -167,16 +167,8 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   }
   K.rz = rz;
   K.ry = ry;
-  static const int envTxt = [] { // tuning experiments only: threads along x (4 points each)
-    const char *e = std::getenv("HG_JIT_TXT");
-    return e ? std::atoi(e) : 0;
-  }();
-  static const int envTyt = [] { // tuning experiments only: rows per tile
-    const char *e = std::getenv("HG_JIT_TYT");
-    return e ? std::atoi(e) : 0;
-  }();
-  K.txt = r == 3 ? (envTxt == 32 ? 32 : 16) : 32;
-  K.tyt = r == 3 ? (envTyt > 0 && (envTyt * K.txt) % 32 == 0 ? envTyt : 16) : 1;
+  K.txt = r == 3 ? 16 : 32;
+  K.tyt = r == 3 ? 16 : 1;
   K.tx = K.txt * 4;
   K.ty = K.tyt;
   const int O = p.noperands;
@@ -188,14 +180,10 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   const int sstride = (stage + ve - 1) / ve * ve;
   // TMA planes in flight beyond the 2RZ+1 window: 6 where shared memory allows (PW set:
   // 214 -> 224 GPts/s from depth 3 to 6, profiles/r1_sweeps.md), down to 1
-  static const int envDepth = [] {
-    const char *e = std::getenv("HG_JIT_DEPTH"); // tuning experiments only
-    return e ? std::max(1, std::atoi(e)) : 0;
-  }();
   // >= 3 operand slabs per plane: a 3-deep ring keeps two CTAs per SM (with 16-plane chunks,
   // jitLaunch; PW set 222-224 -> 230-231 GPts/s, profiles/r1_sweeps.md); fewer operands
   // keep the 6-deep ring
-  const int want = envDepth ? envDepth : (O >= 3 ? 3 : 6);
+  const int want = K.deep > 0 ? K.deep : (O >= 3 ? 3 : 6); // K.deep > 0: HG_JIT_DEPTH
   K.deep = want;
   auto smemFor = [&](int d) {
     return 128 + static_cast<size_t>(es) * (2 * rz + 1 + d) * O * sstride + 2 * (2 * rz + 1 + d) * 8;
@@ -249,10 +237,7 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
     s << "((double2 *)q)[0] = make_double2(r.v[0], r.v[1]); ((double2 *)q)[1] = "
          "make_double2(r.v[2], r.v[3]); ";
   s << "}\n";
-  static const int minBlocks = [] { // tuning experiments only
-    const char *e = std::getenv("HG_JIT_MINB");
-    return e ? std::max(1, std::atoi(e)) : 1;
-  }();
+  constexpr int minBlocks = 1;
   s << "extern \"C\" __global__ void __launch_bounds__(" << K.nthreads << ", " << minBlocks
     << ") hg_apply(const __grid_constant__ P_t P) {\n";
   s << "  constexpr int O = " << O << ", RZ = " << rz << ", RY = " << ry << ", NS = " << K.ns

@@ -18,7 +18,7 @@ struct JitKernel {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   int rz = 0, ry = 0, txt = 16, tyt = 16, tx = 64, ty = 16, ns = 0, ncons = 0, nthreads = 0;
-  int deep = 6; // requested TMA ring depth beyond the 2RZ+1 window (chunk sizing follows it)
+  int deep = 0; // TMA ring depth beyond the 2RZ+1 window (0 = auto; chunk sizing follows it)
   size_t smem = 0;
 };
 

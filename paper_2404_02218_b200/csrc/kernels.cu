@@ -17,6 +17,7 @@
 #include <mutex>
 #include <type_traits>
 #include <utility>
+#include <vector>
 
 // TMA prefetch depth (planes in flight beyond the R+1 a CTA computes on); tunables.
 #ifndef HG_DEPTH3
@@ -27,12 +28,6 @@
 #endif
 #ifndef HG_DEPTH2
 #define HG_DEPTH2 4
-#endif
-#ifndef HG_CLUSTER_Y
-#define HG_CLUSTER_Y 1
-#endif
-#ifndef HG_ORDER
-#define HG_ORDER 0
 #endif
 #ifndef HG_MINB_R4
 #define HG_MINB_R4 1
@@ -54,6 +49,11 @@
 #endif
 
 namespace hg {
+
+UnitOrderCache::~UnitOrderCache() {
+  for (auto &kv : tables)
+    cudaFree(kv.second);
+}
 
 DevLayout devLayout(const Layout &L) {
   DevLayout d{};
@@ -136,17 +136,27 @@ template <typename T> struct StarParams {
   int zs, ys, xs;  // raw start of the output region
   int nz, ny, nx;  // output extents
   int tiles_x, tiles_y, chunk, nchunks;
-  int cy, bands; // cluster size along y and number of y bands (tiles_y / cy, rounded up)
-  int order;     // unit -> (tile, chunk) order
+  // launch order -> unit (chunk * tiles_y + tile_y) * tiles_x + tile_x; the units touching a
+  // halo face come last so their waits overlap the interior (null: natural order)
+  const int *perm;
   // dmp: before loading any halo row of a face whose neighbour exists, the producer waits
   // until that neighbour's put of this step has landed (flag >= epoch, system-scope acquire)
   const unsigned long long *flags;
   unsigned long long epoch;
   int wmask;     // bit 2*dim + (sign > 0): a neighbour sends into that face
+  unsigned long long *err;        // bounded waits (waitFlag)
+  unsigned long long timeout_ns;
+  // packed x faces: slab [y][z][xw] of the cur buffer's lo/hi x halo, unpacked by the
+  // producer warp of the receiving CTAs before their TMA loads
+  T *cur;
+  const T *xin[2];
+  int xw[2];
   // fused swap of the NEXT step: output points inside a send box (width hs[d] at face d) are
-  // also stored into the neighbour's buffer (peer[d] + my index + pdelta[d]); each face's
-  // CTAs count completions and the last one publishes put_epoch to the neighbour's flag
+  // also stored into the neighbour's buffer (peer[d] + my index + pdelta[d]), or for a packed
+  // x face (xpack bit d) into the neighbour's slab peer[d]; each face's CTAs count completions
+  // and the last one publishes put_epoch to the neighbour's flag
   int fuse;
+  int xpack;
   int hs[6];
   T *peer[6];
   int64_t pdelta[6];
@@ -154,7 +164,6 @@ template <typename T> struct StarParams {
   unsigned int cnt_target[6];
   unsigned long long *peer_flag[6];
   unsigned long long put_epoch;
-  int boundary_last;
   T *out;
   T w0, wz[3], wy[3], wx[3], scale, two;
   // f32 packed path: the same weights as {w, w} pairs (uniform registers) and a zero that
@@ -209,36 +218,12 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   uint64_t *full = reinterpret_cast<uint64_t *>(pstages + (C::WAVE ? size_t(NS) * C::PSTAGE : 0));
   uint64_t *empty = full + NS;
 
-  // unit -> (tile, chunk); optionally the z-boundary chunks go last
-  // unit -> (y-member of a cluster, x tile, y band, z chunk); the cy CTAs of one cluster are
-  // the y-adjacent tiles of one column band, gang-scheduled so their shared halo rows are
-  // fetched from HBM once and hit in L2 for the neighbour
-  int u = blockIdx.x;
-  int txi, tyi, chunk;
-  if (P.order == 0) {
-    const int mem = u % P.cy;
-    u /= P.cy;
-    txi = u % P.tiles_x;
-    u /= P.tiles_x;
-    tyi = (u % P.bands) * P.cy + mem;
-    chunk = u / P.bands;
-  } else if (P.order == 1) { // chunk fastest: the z-chunks of one column tile run together
-    chunk = u % P.nchunks;
-    u /= P.nchunks;
-    txi = u % P.tiles_x;
-    tyi = u / P.tiles_x;
-  } else { // chunk fastest within 4x4 groups of column tiles
-    chunk = u % P.nchunks;
-    u /= P.nchunks;
-    const int g = u / 16, w = u % 16;
-    const int gx = (P.tiles_x + 3) / 4;
-    txi = (g % gx) * 4 + (w % 4);
-    tyi = (g / gx) * 4 + (w / 4);
-    if (txi >= P.tiles_x)
-      tyi = P.tiles_y; // padding unit: no work
-  }
-  if (P.boundary_last && P.nchunks > 2)
-    chunk = chunk < P.nchunks - 2 ? chunk + 1 : (chunk == P.nchunks - 2 ? 0 : P.nchunks - 1);
+  // unit -> (x tile, y tile, z chunk), x fastest
+  int u = P.perm ? __ldg(P.perm + blockIdx.x) : int(blockIdx.x);
+  const int txi = u % P.tiles_x;
+  u /= P.tiles_x;
+  const int tyi = u % P.tiles_y;
+  const int chunk = u / P.tiles_y;
   const int xb = txi * C::TX, yb = tyi * C::TY;
   const int zb = chunk * P.chunk;
   const int n = tyi < P.tiles_y ? min(P.chunk, P.nz - zb) : 0;
@@ -257,32 +242,53 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
 
   if (tid >= C::NCONS) {
     // ---------------- producer warp ----------------
-    if (tid == C::NCONS) {
+    const int plane_lane = tid - C::NCONS;
+    if (P.flags) {
+      constexpr int XD = RANK - 1;
+      int need = 0;
+      if (zb == 0) need |= 1;
+      if (zb + n >= P.nz) need |= 2;
+      if (RANK == 3 && yb == 0) need |= 4;
+      if (RANK == 3 && yb + C::TY >= P.ny) need |= 8;
+      if (xb == 0) need |= 1 << (2 * XD);
+      if (xb + C::TX >= P.nx) need |= 2 << (2 * XD);
+      need &= P.wmask;
+      if (plane_lane == 0)
+        for (int di = 0; di < 6; ++di)
+          if (need & (1 << di))
+            waitFlag(P.flags + di, P.epoch, P.err, P.timeout_ns,
+                     (P.epoch << 8) | (unsigned long long)(di << 1) | 1ull);
+      __syncwarp();
+      // packed x faces: the whole warp unpacks the slab rows this CTA's boxes read (its rows
+      // and y rim, its planes and z rim, clipped to the core) into the halo columns
+#pragma unroll 1
+      for (int sd = 0; sd < 2; ++sd) {
+        if (!(need & (1 << (2 * XD + sd))) || !P.xin[sd])
+          continue;
+        const T *slab = P.xin[sd];
+        const int W = P.xw[sd];
+        const int y0 = RANK == 3 ? max(0, yb - RY) : 0;
+        const int y1 = RANK == 3 ? min(P.ny, yb + C::TY + RY) : 1;
+        const int z0 = max(0, zb - R), z1 = min(P.nz, zb + n + R);
+        const int per = (z1 - z0) * W;
+        const int64_t xoff = sd ? int64_t(P.nx) : -int64_t(W);
+        for (int y = y0; y < y1; ++y) {
+          const T *src = slab + (int64_t(y) * P.nz + z0) * W;
+          T *dst = P.cur + int64_t(P.zs + z0) * P.plane +
+                   (RANK == 3 ? int64_t(P.ys + y) * P.pitch : 0) + P.col0 + P.xs + xoff;
+          for (int k = plane_lane; k < per; k += 32) {
+            const int dz = k / W;
+            dst[int64_t(dz) * P.plane + (k - dz * W)] = src[k];
+          }
+        }
+      }
+      // the halo bytes arrived through the generic proxy; TMA reads via the async proxy
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
+    }
+    if (plane_lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur))
                    : "memory");
-      if (P.flags) {
-        constexpr int XD = RANK - 1;
-        int need = 0;
-        if (zb == 0) need |= 1;
-        if (zb + n >= P.nz) need |= 2;
-        if (RANK == 3 && yb == 0) need |= 4;
-        if (RANK == 3 && yb + C::TY >= P.ny) need |= 8;
-        if (xb == 0) need |= 1 << (2 * XD);
-        if (xb + C::TX >= P.nx) need |= 2 << (2 * XD);
-        need &= P.wmask;
-        for (int di = 0; di < 6; ++di)
-          if (need & (1 << di)) {
-            unsigned long long v;
-            do {
-              asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
-                           : "=l"(v)
-                           : "l"(P.flags + di)
-                           : "memory");
-            } while (v < P.epoch);
-          }
-        // the halo bytes arrived through the generic proxy; TMA reads via the async proxy
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
       const int cx = int(P.col0) + P.xs + xb - C::PADX;
       const int cy = RANK == 3 ? P.ys + yb - RY : 0;
       const int z0 = P.zs + zb - R;
@@ -548,7 +554,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       const T *src = outRow;
       const int64_t e0 = outRow - P.out;
       for (int d = 0; d < 2 * RANK; ++d) {
-        if (!(blockTouch & (1 << d)))
+        if (!(blockTouch & (1 << d)) || (P.xpack & (1 << d)))
           continue;
         const int dim = d >> 1;
         const bool lo = (d & 1) == 0;
@@ -595,6 +601,46 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         }
       }
     }
+    if (blockTouch & P.xpack) {
+      // packed x faces: the CTA's rows of the face as slab segments [y][z0..z0+n)[W],
+      // contiguous per row, written by all consumer threads in 16-byte stores (each reads the
+      // points back from the output rows the CTA just stored; the barrier orders them)
+      asm volatile("bar.sync 1, %0;" ::"r"(C::NCONS) : "memory");
+      constexpr int XD = RANK - 1;
+      const int ny0 = RANK == 3 ? yb : 0;
+      const int nrows = RANK == 3 ? min(C::TY, P.ny - yb) : 1;
+#pragma unroll 1
+      for (int d = 2 * XD; d < 2 * XD + 2; ++d) {
+        if (!(blockTouch & P.xpack & (1 << d)))
+          continue;
+        const int W = P.hs[d];
+        const int xlo = (d & 1) ? P.nx - W : 0;
+        const int per = n * W, gpr = (per + 3) / 4;
+        T *slab = P.peer[d];
+        for (int g = tid; g < nrows * gpr; g += C::NCONS) {
+          const int r = g / gpr, k0 = (g - r * gpr) * 4;
+          const int y = ny0 + r;
+          const T *src = P.out + int64_t(P.zs + zb) * P.plane +
+                         (RANK == 3 ? int64_t(P.ys + y) * P.pitch : 0) + P.col0 + P.xs + xlo;
+          T *dst = slab + (int64_t(y) * P.nz + zb) * W + k0;
+          T v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = k0 + j;
+            const int dz = k / W;
+            v[j] = k < per ? src[int64_t(dz) * P.plane + (k - dz * W)] : T(0);
+          }
+          if (k0 + 4 <= per && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            st4(dst, V4<T>{{v[0], v[1], v[2], v[3]}});
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (k0 + j < per)
+                dst[j] = v[j];
+          }
+        }
+      }
+    }
     // publish: every face this CTA fed is counted; the last CTA of a face releases the epoch
     __threadfence_system();
     asm volatile("bar.sync 1, %0;" ::"r"(C::NCONS) : "memory");
@@ -610,6 +656,64 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
           }
         }
   }
+}
+
+// Launch order of the star units with every unit that touches a face in bmask (bit
+// 2*dim + hi; dims z, [y], x) after all the others, natural order within each group.  Built
+// once per geometry and cached by the plan; null (natural order) inside a stream capture.
+int unitOrder(UnitOrderCache &cache, int bmask, int rank, int tiles_x, int tiles_y, int nchunks,
+              int TX, int TY, int chunk, int nx, int ny, int nz, cudaStream_t st,
+              const int **perm, int *ninner) {
+  *perm = nullptr;
+  *ninner = 0;
+  const std::string key = std::to_string(bmask) + "/" + std::to_string(rank) + "/" +
+                          std::to_string(tiles_x) + "/" + std::to_string(tiles_y) + "/" +
+                          std::to_string(nchunks) + "/" + std::to_string(TX) + "/" +
+                          std::to_string(TY) + "/" + std::to_string(chunk);
+  auto it = cache.tables.find(key);
+  if (it != cache.tables.end()) {
+    *perm = it->second;
+    *ninner = cache.inner[key];
+    return HG_OK;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return HG_OK;
+  }
+  const int xd = rank - 1;
+  std::vector<int> inner, outer;
+  const long total = long(tiles_x) * tiles_y * nchunks;
+  inner.reserve(size_t(total));
+  for (int c = 0; c < nchunks; ++c)
+    for (int ty = 0; ty < tiles_y; ++ty)
+      for (int tx = 0; tx < tiles_x; ++tx) {
+        int m = 0;
+        if (c == 0) m |= 1;
+        if ((c + 1) * chunk >= nz) m |= 2;
+        if (rank == 3 && ty == 0) m |= 4;
+        if (rank == 3 && (ty + 1) * TY >= ny) m |= 8;
+        if (tx == 0) m |= 1 << (2 * xd);
+        if ((tx + 1) * TX >= nx) m |= 2 << (2 * xd);
+        const int u = (c * tiles_y + ty) * tiles_x + tx;
+        (m & bmask ? outer : inner).push_back(u);
+      }
+  const int nin = int(inner.size());
+  inner.insert(inner.end(), outer.begin(), outer.end());
+  int *d = nullptr;
+  if (cudaMalloc(&d, inner.size() * sizeof(int)) != cudaSuccess)
+    return cudaErr(cudaGetLastError(), "cudaMalloc(unit order)");
+  const cudaError_t e =
+      cudaMemcpy(d, inner.data(), inner.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return cudaErr(e, "cudaMemcpy(unit order)");
+  }
+  cache.tables[key] = d;
+  cache.inner[key] = nin;
+  *perm = d;
+  *ninner = nin;
+  return HG_OK;
 }
 
 template <typename T, int RANK, int NT, int KIND, int GEO = 0>
@@ -678,11 +782,18 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   }
   P.chunk = (P.nz + chunks - 1) / chunks;
   P.nchunks = (P.nz + P.chunk - 1) / P.chunk;
-  P.boundary_last = L.zorder_boundary_last;
   P.flags = L.wait_flags;
   P.epoch = L.wait_epoch;
   P.wmask = L.wait_mask;
+  P.err = L.err;
+  P.timeout_ns = L.timeout_ns;
+  P.cur = static_cast<T *>(L.cur);
+  for (int sd = 0; sd < 2; ++sd) {
+    P.xin[sd] = static_cast<const T *>(L.xin[sd]);
+    P.xw[sd] = L.xw[sd];
+  }
   P.fuse = L.fuse;
+  unsigned targets[6] = {0, 0, 0, 0, 0, 0};
   if (L.fuse) {
     // CTAs whose output region meets each face's send box (the kernel's blockTouch)
     auto touching = [](int ext, int tile, int ntl, int h, bool lo) {
@@ -695,6 +806,7 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
       return c;
     };
     const int nyt = RANK == 3 ? P.tiles_y : 1;
+    P.xpack = L.xpack;
     for (int d = 0; d < 6; ++d) {
       P.hs[d] = L.hs[d];
       P.peer[d] = static_cast<T *>(L.peer[d]);
@@ -711,8 +823,9 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
         c = long(touching(P.ny, C::TY, P.tiles_y, L.hs[d], lo)) * P.tiles_x * P.nchunks;
       else
         c = long(touching(P.nx, C::TX, P.tiles_x, L.hs[d], lo)) * nyt * P.nchunks;
-      L.cnt_accum[d] += unsigned(c);
-      P.cnt_target[d] = L.cnt_accum[d];
+      // cumulative per-face target; committed to the host mirror only once the launch is in
+      targets[d] = L.cnt_accum[d] + unsigned(c);
+      P.cnt_target[d] = targets[d];
     }
     P.cnt = L.cnt;
     P.put_epoch = L.put_epoch;
@@ -738,42 +851,56 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
     P.ptwo = pair(s.two);
     P.zero = 0;
   }
-  P.cy = 1;
-  if (RANK == 3) {
-    P.cy = HG_CLUSTER_Y;
-    if (const char *e = std::getenv("HG_CLUSTER")) // tuning experiments only
-      P.cy = std::max(1, std::atoi(e));
-    P.cy = std::min(P.cy, P.tiles_y);
+  // launch order: the units touching a face that waits for a halo or sends one go last, so
+  // their waits (and the peers' flags, published at the end of the peers' previous step)
+  // overlap the interior units
+  int bmask = L.wait_mask | L.split_mask;
+  for (int d = 0; d < 6; ++d)
+    if (L.fuse && L.hs[d])
+      bmask |= 1 << d;
+  if (L.zorder_boundary_last)
+    bmask |= 3;
+  P.perm = nullptr;
+  const unsigned blocks = unsigned(P.tiles_x) * P.tiles_y * P.nchunks;
+  int ninner = int(blocks);
+  if (bmask && L.order) {
+    int rc = unitOrder(*L.order, bmask, RANK, P.tiles_x, P.tiles_y, P.nchunks, C::TX, C::TY,
+                       P.chunk, P.nx, P.ny, P.nz, st, &P.perm, &ninner);
+    if (rc)
+      return rc;
   }
-  P.bands = (P.tiles_y + P.cy - 1) / P.cy;
-  P.order = HG_ORDER;
-  if (const char *e = std::getenv("HG_ORDER")) // tuning experiments only
-    P.order = std::atoi(e);
-  if (P.cy > 1)
-    P.order = 0;
-  unsigned blocks = unsigned(P.cy) * P.tiles_x * P.bands * P.nchunks;
-  if (P.order == 2)
-    blocks = unsigned((P.tiles_x + 3) / 4) * ((P.tiles_y + 3) / 4) * 16 * P.nchunks;
   if (blocks_out)
     *blocks_out = int(blocks);
-  if (P.cy == 1) {
+  int rc;
+  if (L.split_event && P.perm) {
+    // the interior units, then (once the halos are in) the units that read them
+    if (ninner > 0)
+      kern<<<unsigned(ninner), C::NTHREADS, C::SMEM, st>>>(*L.tm_cur, *L.tm_prev, P);
+    rc = cudaErr(cudaGetLastError(), "star kernel launch (interior)");
+    if (rc)
+      return rc;
+    rc = cudaErr(cudaStreamWaitEvent(st, L.split_event, 0), "cudaStreamWaitEvent(halo)");
+    if (rc)
+      return rc;
+    StarParams<T> Q = P;
+    Q.perm = P.perm + ninner;
+    if (blocks > unsigned(ninner))
+      kern<<<blocks - unsigned(ninner), C::NTHREADS, C::SMEM, st>>>(*L.tm_cur, *L.tm_prev, Q);
+    rc = cudaErr(cudaGetLastError(), "star kernel launch (boundary)");
+  } else {
+    if (L.split_event) {
+      rc = cudaErr(cudaStreamWaitEvent(st, L.split_event, 0), "cudaStreamWaitEvent(halo)");
+      if (rc)
+        return rc;
+    }
     kern<<<blocks, C::NTHREADS, C::SMEM, st>>>(*L.tm_cur, *L.tm_prev, P);
-    return cudaErr(cudaGetLastError(), "star kernel launch");
+    rc = cudaErr(cudaGetLastError(), "star kernel launch");
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(C::NTHREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = unsigned(P.cy);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaErr(cudaLaunchKernelEx(&cfg, kern, *L.tm_cur, *L.tm_prev, P),
-                 "star kernel cluster launch");
+  if (rc == HG_OK && L.fuse)
+    for (int d = 0; d < 6; ++d)
+      if (L.hs[d])
+        L.cnt_accum[d] = targets[d];
+  return rc;
 }
 
 template <typename T, int RANK, int NT, int KIND> int residentT() {
@@ -1067,7 +1194,6 @@ __global__ void packKernel(T *base, const DevLayout L, int64_t a0, int64_t a1, i
 struct PutParams {
   PutJob jobs[96];
   int njobs;
-  DevLayout L;
   unsigned long long *flags[2 * HG_MAX_RANK];
   int nflags;
   unsigned long long epoch;
@@ -1084,57 +1210,79 @@ __device__ __forceinline__ int64_t boxElem(const DevLayout &L, const int64_t *at
 }
 
 // Fused pack + NVLink store + unpack: each face box of my buffer is written straight into the
-// neighbour's receive box (peer-mapped), byte-exact.  The last CTA to finish publishes the
-// epoch to every neighbour's flag with a system-scope release.
+// neighbour's receive box (peer-mapped), byte-exact -- or, for a packed x face, into the
+// neighbour's receive slab (the box as [y][z][x] for rank 3, [z][x] for rank 2), which its
+// stencil kernel unpacks.  Each job carries its own field's layout.  The last CTA to finish
+// publishes the epoch to every neighbour's flag with a system-scope release.
 template <typename T> __global__ void putKernel(const __grid_constant__ PutParams P) {
   const PutJob &J = P.jobs[blockIdx.y];
+  const DevLayout &L = J.lay;
   // rows of the box (all dims but the last) x contiguous width (the last dim)
-  const int64_t rowsEff = P.L.rank == 3 ? J.size[0] * J.size[1] : (P.L.rank == 2 ? J.size[0] : 1);
-  const int64_t w = P.L.rank == 3 ? J.size[2] : (P.L.rank == 2 ? J.size[1] : J.size[0]);
+  const int64_t rowsEff = L.rank == 3 ? J.size[0] * J.size[1] : (L.rank == 2 ? J.size[0] : 1);
+  const int64_t w = L.rank == 3 ? J.size[2] : (L.rank == 2 ? J.size[1] : J.size[0]);
   const T *src = static_cast<const T *>(J.src);
   T *dst = static_cast<T *>(J.dst);
-  // 16-byte path when both rows start 16-byte aligned (z/y faces: rows of the core width,
-  // starting at the 128-byte-aligned core column)
-  constexpr int VE = 16 / sizeof(T);
-  const int64_t lastS = P.L.rank == 3 ? J.src_at[2] : (P.L.rank == 2 ? J.src_at[1] : J.src_at[0]);
-  const int64_t lastD = P.L.rank == 3 ? J.dst_at[2] : (P.L.rank == 2 ? J.dst_at[1] : J.dst_at[0]);
-  const bool vec = P.L.rank >= 2 && w % VE == 0 && (P.L.col0 + lastS) % VE == 0 &&
-                   (P.L.col0 + lastD) % VE == 0 && P.L.pitch % VE == 0;
-  if (vec) {
-    for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
-      int64_t i0 = P.L.rank == 3 ? r / J.size[1] : r, i1 = P.L.rank == 3 ? r % J.size[1] : 0;
-      const int64_t se = P.L.rank == 3 ? boxElem(P.L, J.src_at, i0, i1, 0)
-                                       : boxElem(P.L, J.src_at, i0, 0, 0);
-      const int64_t de = P.L.rank == 3 ? boxElem(P.L, J.dst_at, i0, i1, 0)
-                                       : boxElem(P.L, J.dst_at, i0, 0, 0);
-      const int4 *s4 = reinterpret_cast<const int4 *>(src + se);
-      int4 *d4 = reinterpret_cast<int4 *>(dst + de);
-      for (int64_t c = threadIdx.x; c < w / VE; c += blockDim.x)
-        d4[c] = s4[c];
-    }
-  } else
-  for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
-    int64_t i0, i1;
-    if (P.L.rank == 3) {
-      i0 = r / J.size[1];
-      i1 = r % J.size[1];
-    } else {
-      i0 = r;
-      i1 = 0;
-    }
-    for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
-      int64_t se, de;
-      if (P.L.rank == 3) {
-        se = boxElem(P.L, J.src_at, i0, i1, c);
-        de = boxElem(P.L, J.dst_at, i0, i1, c);
-      } else if (P.L.rank == 2) {
-        se = boxElem(P.L, J.src_at, i0, c, 0);
-        de = boxElem(P.L, J.dst_at, i0, c, 0);
+  if (J.packed) {
+    // element k of the send box (row-major z, y, x) -> slab [y][z][x]
+    const int64_t total = rowsEff * w;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
+         k += int64_t(gridDim.x) * blockDim.x) {
+      const int64_t i2 = k % w, r = k / w;
+      int64_t i0 = r, i1 = 0, o;
+      if (L.rank == 3) {
+        i0 = r / J.size[1];
+        i1 = r % J.size[1];
+        o = (i1 * J.size[0] + i0) * w + i2;
       } else {
-        se = boxElem(P.L, J.src_at, c, 0, 0);
-        de = boxElem(P.L, J.dst_at, c, 0, 0);
+        o = r * w + i2;
       }
-      dst[de] = src[se];
+      dst[o] = src[L.rank == 3 ? boxElem(L, J.src_at, i0, i1, i2) : boxElem(L, J.src_at, i0, i2, 0)];
+    }
+  } else {
+    // 16-byte path when both rows start 16-byte aligned (z/y faces: rows of the core width,
+    // starting at the 128-byte-aligned core column)
+    constexpr int VE = 16 / sizeof(T);
+    const int64_t lastS = L.rank == 3 ? J.src_at[2] : (L.rank == 2 ? J.src_at[1] : J.src_at[0]);
+    const int64_t lastD = L.rank == 3 ? J.dst_at[2] : (L.rank == 2 ? J.dst_at[1] : J.dst_at[0]);
+    const bool vec = L.rank >= 2 && w % VE == 0 && (L.col0 + lastS) % VE == 0 &&
+                     (L.col0 + lastD) % VE == 0 && L.pitch % VE == 0;
+    if (vec) {
+      for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
+        int64_t i0 = L.rank == 3 ? r / J.size[1] : r, i1 = L.rank == 3 ? r % J.size[1] : 0;
+        const int64_t se = L.rank == 3 ? boxElem(L, J.src_at, i0, i1, 0)
+                                       : boxElem(L, J.src_at, i0, 0, 0);
+        const int64_t de = L.rank == 3 ? boxElem(L, J.dst_at, i0, i1, 0)
+                                       : boxElem(L, J.dst_at, i0, 0, 0);
+        const int4 *s4 = reinterpret_cast<const int4 *>(src + se);
+        int4 *d4 = reinterpret_cast<int4 *>(dst + de);
+        for (int64_t c = threadIdx.x; c < w / VE; c += blockDim.x)
+          d4[c] = s4[c];
+      }
+    } else {
+      for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
+        int64_t i0, i1;
+        if (L.rank == 3) {
+          i0 = r / J.size[1];
+          i1 = r % J.size[1];
+        } else {
+          i0 = r;
+          i1 = 0;
+        }
+        for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
+          int64_t se, de;
+          if (L.rank == 3) {
+            se = boxElem(L, J.src_at, i0, i1, c);
+            de = boxElem(L, J.dst_at, i0, i1, c);
+          } else if (L.rank == 2) {
+            se = boxElem(L, J.src_at, i0, c, 0);
+            de = boxElem(L, J.dst_at, i0, c, 0);
+          } else {
+            se = boxElem(L, J.src_at, c, 0, 0);
+            de = boxElem(L, J.dst_at, c, 0, 0);
+          }
+          dst[de] = src[se];
+        }
+      }
     }
   }
   if (P.nflags == 0)
@@ -1154,15 +1302,30 @@ template <typename T> __global__ void putKernel(const __grid_constant__ PutParam
   }
 }
 
-__global__ void waitKernel(const unsigned long long *flags, int i0, int i1, int i2, int i3,
-                           int i4, int i5, int n, unsigned long long epoch) {
-  const int idx[6] = {i0, i1, i2, i3, i4, i5};
-  for (int k = 0; k < n; ++k) {
-    unsigned long long v;
-    do {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + idx[k]) : "memory");
-    } while (v < epoch);
+struct WaitParams {
+  const unsigned long long *flags;
+  int idx[6];
+  int n;
+  unsigned long long epoch;
+  unsigned long long *err;
+  unsigned long long timeout_ns;
+  // ready handshake only: peers' ready words to publish into first
+  unsigned long long *peer[6];
+  int npeer;
+};
+
+// Lane k waits for flags[idx[k]] >= epoch (bounded, waitFlag); with npeer > 0 the lanes
+// first publish epoch into the peers' words (system-scope release).
+__global__ void waitKernel(const __grid_constant__ WaitParams P) {
+  const int k = threadIdx.x;
+  if (k < P.npeer) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.peer[k]), "l"(P.epoch) : "memory");
   }
+  if (k < P.n)
+    waitFlag(P.flags + P.idx[k], P.epoch, P.err, P.timeout_ns,
+             (P.epoch << 8) | (unsigned long long)(P.idx[k] << 1) | 1ull);
+  __syncwarp();
   __threadfence_system();
 }
 
@@ -1209,8 +1372,6 @@ int makeBoxTensorMap(int dtype, const DevLayout &lay, void *base, const uint32_t
 }
 
 int starGeoFor(const StarSpec &s, int dtype, int rank, const int64_t *ext) {
-  if (const char *e = std::getenv("HG_STAR_GEO")) // A/B experiments only
-    return rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2 ? std::atoi(e) : 0;
   // wide tiles pay on large planes (>= 768 x 768); 512^2 planes prefer the 64 x 16 tile
   return rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2 && ext[1] >= 768 &&
                  ext[2] >= 768
@@ -1253,12 +1414,7 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
   const CUtensorMapDataType dt =
       dtype == HG_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   cuuint32_t boxCur[3] = {cuuint32_t(TX + 8), cuuint32_t(TY + 2 * RY), cuuint32_t(HG_ZP)};
-  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  if (const char *e = std::getenv("HG_L2PROMO")) // tuning experiments only
-    promo = e[0] == '0' ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-            : e[0] == '1' ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-            : e[0] == '2' ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-                          : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+  const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = encode(cur, dt, 3, base, dims, strides, boxCur, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -1433,7 +1589,7 @@ int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const 
   return cudaErr(cudaGetLastError(), "pack kernel launch");
 }
 
-int launchPut(const PutJob *jobs, int njobs, const DevLayout &lay, const PutSignal *sig, int nsig,
+int launchPut(const PutJob *jobs, int njobs, const PutSignal *sig, int nsig,
               unsigned long long epoch, unsigned int *counter, cudaStream_t st) {
   PutParams P{};
   if (njobs > 96)
@@ -1441,7 +1597,6 @@ int launchPut(const PutJob *jobs, int njobs, const DevLayout &lay, const PutSign
   for (int j = 0; j < njobs; ++j)
     P.jobs[j] = jobs[j];
   P.njobs = njobs;
-  P.L = lay;
   P.nflags = 0;
   for (int f = 0; f < nsig; ++f)
     if (sig[f].flag)
@@ -1451,17 +1606,23 @@ int launchPut(const PutJob *jobs, int njobs, const DevLayout &lay, const PutSign
   if (njobs == 0 && P.nflags == 0)
     return HG_OK;
   int64_t maxRows = 1;
+  int es = 4;
   for (int j = 0; j < njobs; ++j) {
-    int64_t rows = lay.rank == 3 ? jobs[j].size[0] * jobs[j].size[1]
-                                 : (lay.rank == 2 ? jobs[j].size[0] : 1);
-    maxRows = std::max(maxRows, rows);
+    const DevLayout &L = jobs[j].lay;
+    const int64_t rows = L.rank == 3 ? jobs[j].size[0] * jobs[j].size[1]
+                                     : (L.rank == 2 ? jobs[j].size[0] : 1);
+    // packed jobs run one element per thread: rows of 256 elements
+    maxRows = std::max(maxRows, jobs[j].packed ? (rows * jobs[j].size[L.rank - 1] + 255) / 256
+                                               : rows);
+    es = L.es;
   }
   dim3 grid(unsigned(std::min<int64_t>(maxRows, 1184)), unsigned(std::max(njobs, 1)));
   if (njobs == 0) { // flags only: a single CTA with no copy work
     P.jobs[0] = PutJob{};
+    P.jobs[0].lay.rank = 1;
     grid = dim3(1, 1);
   }
-  if (lay.es == 4)
+  if (es == 4)
     putKernel<float><<<grid, 256, 0, st>>>(P);
   else
     putKernel<double><<<grid, 256, 0, st>>>(P);
@@ -1469,14 +1630,41 @@ int launchPut(const PutJob *jobs, int njobs, const DevLayout &lay, const PutSign
 }
 
 int launchWaitFlags(const unsigned long long *flags, const int *idx, int n,
-                    unsigned long long epoch, cudaStream_t st) {
+                    unsigned long long epoch, unsigned long long *err,
+                    unsigned long long timeout_ns, cudaStream_t st) {
   if (n <= 0)
     return HG_OK;
-  int i[6] = {0, 0, 0, 0, 0, 0};
-  for (int k = 0; k < n && k < 6; ++k)
-    i[k] = idx[k];
-  waitKernel<<<1, 1, 0, st>>>(flags, i[0], i[1], i[2], i[3], i[4], i[5], n, epoch);
+  WaitParams P{};
+  P.flags = flags;
+  P.n = std::min(n, 6);
+  for (int k = 0; k < P.n; ++k)
+    P.idx[k] = idx[k];
+  P.epoch = epoch;
+  P.err = err;
+  P.timeout_ns = timeout_ns;
+  waitKernel<<<1, 32, 0, st>>>(P);
   return cudaErr(cudaGetLastError(), "wait kernel launch");
+}
+
+int launchReady(unsigned long long *const *peer_ready, int npeer,
+                const unsigned long long *ready, const int *idx, int n,
+                unsigned long long epoch, unsigned long long *err,
+                unsigned long long timeout_ns, cudaStream_t st) {
+  WaitParams P{};
+  P.flags = ready;
+  P.n = std::min(n, 6);
+  for (int k = 0; k < P.n; ++k)
+    P.idx[k] = idx[k];
+  P.npeer = std::min(npeer, 6);
+  for (int k = 0; k < P.npeer; ++k)
+    P.peer[k] = peer_ready[k];
+  P.epoch = epoch;
+  P.err = err;
+  P.timeout_ns = timeout_ns;
+  if (P.n == 0 && P.npeer == 0)
+    return HG_OK;
+  waitKernel<<<1, 32, 0, st>>>(P);
+  return cudaErr(cudaGetLastError(), "ready kernel launch");
 }
 
 } // namespace hg

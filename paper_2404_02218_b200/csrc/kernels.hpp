@@ -7,6 +7,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <string>
+
 namespace hg {
 
 // Device view of one buffer's layout (see makeLayout).
@@ -22,6 +25,13 @@ struct DevLayout {
 DevLayout devLayout(const Layout &L);
 
 // ---- star family (TMA-pipelined, register-streamed along dim 0) -------------------------
+// Device tables mapping launch order -> (tile, chunk) unit with the units that touch a halo
+// face last, cached per (face mask, geometry); owned by a plan.
+struct UnitOrderCache {
+  std::map<std::string, int *> tables;
+  std::map<std::string, int> inner; // units before the first boundary unit
+  ~UnitOrderCache();
+};
 struct StarLaunch {
   const StarSpec *spec;
   int dtype;
@@ -36,11 +46,22 @@ struct StarLaunch {
   int chunks;                 // z-chunks (0 = auto)
   int zorder_boundary_last;   // process z-boundary chunks last (dmp overlap)
   int geo = 0;                // tile geometry (starGeoFor); the tensor maps must match
+  UnitOrderCache *order = nullptr; // plan-owned unit tables (boundary units last)
   const unsigned long long *wait_flags = nullptr; // dmp: my flag words (null = no wait)
   unsigned long long wait_epoch = 0;
   int wait_mask = 0;
+  // bounded waits: after timeout_ns (0 = never) a waiter records (epoch << 8 | face << 1 | 1)
+  // in *err and goes on (the host reports HG_ETRAP instead of the GPU hanging)
+  unsigned long long *err = nullptr;
+  unsigned long long timeout_ns = 0;
+  // packed x faces (the last dim): halo columns arrive as a packed slab [y][z][w] that the
+  // receiving CTAs' producer warp unpacks into the cur buffer before its TMA loads
+  void *cur = nullptr;          // base of the buffer bound to the cur operand
+  const void *xin[2] = {};      // my receive slabs of that buffer (lo, hi x face), or null
+  int xw[2] = {0, 0};           // their widths
   // fused swap of the next step (see StarParams in kernels.cu); cnt_accum is host state
   int fuse = 0;
+  int xpack = 0;                // bit d: face d is sent packed into the peer's slab peer[d]
   int hs[6] = {0, 0, 0, 0, 0, 0};
   void *peer[6] = {};
   int64_t pdelta[6] = {0, 0, 0, 0, 0, 0};
@@ -48,6 +69,10 @@ struct StarLaunch {
   unsigned int *cnt_accum = nullptr;
   unsigned long long *peer_flag[6] = {};
   unsigned long long put_epoch = 0;
+  // split launch (NCCL transport): the units not touching split_mask's faces first, then a
+  // wait for split_event on the stream, then the rest
+  cudaEvent_t split_event = nullptr;
+  int split_mask = 0;
 };
 // Creates the TMA descriptor of a buffer for the star family's cur/prev boxes.
 int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &lay,
@@ -125,18 +150,29 @@ int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const 
 // ---- halo put (fused pack + NVLink store + unpack) + flags --------------------------------
 struct PutJob {
   const void *src;    // my buffer base
-  void *dst;          // neighbour's buffer base (peer-mapped)
+  void *dst;          // neighbour's buffer base (peer-mapped), or its packed receive slab
   int64_t src_at[3];  // raw send box origin
-  int64_t dst_at[3];  // raw receive box origin in the neighbour
+  int64_t dst_at[3];  // raw receive box origin in the neighbour (unused when packed)
   int64_t size[3];
+  DevLayout lay;      // layout of this field (the neighbour's buffer has the same)
+  int packed;         // 1: dst is a slab [y][z][x] of the box (packed x face, rank 3) /
+                      //    [z][x] (rank 2)
 };
 struct PutSignal {
   unsigned long long *flag; // neighbour's flag word (peer-mapped), null = none
 };
-int launchPut(const PutJob *jobs, int njobs, const DevLayout &lay, const PutSignal *sig,
-              int nsig, unsigned long long epoch, unsigned int *counter, cudaStream_t st);
+int launchPut(const PutJob *jobs, int njobs, const PutSignal *sig, int nsig,
+              unsigned long long epoch, unsigned int *counter, cudaStream_t st);
+// bounded waits (timeout_ns 0 = none): see StarLaunch::err
 int launchWaitFlags(const unsigned long long *flags, const int *idx, int n,
-                    unsigned long long epoch, cudaStream_t st);
+                    unsigned long long epoch, unsigned long long *err,
+                    unsigned long long timeout_ns, cudaStream_t st);
+// receiver-ready handshake: publish `epoch` into each peer's ready word (peer_ready[k]),
+// then wait until my ready words ready[idx[k]] reached it
+int launchReady(unsigned long long *const *peer_ready, int npeer,
+                const unsigned long long *ready, const int *idx, int n,
+                unsigned long long epoch, unsigned long long *err,
+                unsigned long long timeout_ns, cudaStream_t st);
 
 } // namespace hg
 

@@ -21,10 +21,11 @@ int cudaCheck(cudaError_t e, const char *what) {
 namespace {
 
 // Generated kernels are cached per (source, device): NVRTC runs once per distinct program.
-std::shared_ptr<JitKernel> jitCached(const hg_program &g, int device) {
+std::shared_ptr<JitKernel> jitCached(const hg_program &g, int device, int depth) {
   static std::mutex mu;
   static std::map<std::pair<std::string, int>, std::shared_ptr<JitKernel>> cache;
   auto k = std::make_shared<JitKernel>();
+  k->deep = depth;
   if (jitBuildSource(g, *k) != HG_OK)
     return nullptr;
   std::lock_guard<std::mutex> lk(mu);
@@ -144,7 +145,7 @@ bool compileMultiJit(hg_plan &p, int device, int &st) {
   st = HG_OK;
   const hg_program &g = p.prog;
   const int F = g.nfields;
-  if (std::getenv("HG_NO_APPLY_JIT") || F + g.ntemps > HG_MAX_FIELDS || g.rank < 2)
+  if (p.knobs.noApplyJit || F + g.ntemps > HG_MAX_FIELDS || g.rank < 2)
     return false;
   for (int f = 1; f < F; ++f)
     for (int d = 0; d < g.rank; ++d)
@@ -182,7 +183,7 @@ bool compileMultiJit(hg_plan &p, int device, int &st) {
       S.store_field[k] = F + t;
       S.store[k] = A.domain;
       if (consumers[static_cast<size_t>(t)] == 0 && stores[static_cast<size_t>(t)] == 1 &&
-          !std::getenv("HG_MULTI_NODIRECT") && jitMisaligned(S, p.lay[0]) == 0)
+          jitMisaligned(S, p.lay[0]) == 0)
         for (int j = 0; j < g.nstores; ++j)
           if (g.mstore_temp[j] == t && sameBox(g.mstore[j], A.domain, g.rank)) {
             M.direct[static_cast<size_t>(k)] = g.mstore_field[j];
@@ -192,7 +193,7 @@ bool compileMultiJit(hg_plan &p, int device, int &st) {
     Analysis none;
     if (!jitEligible(S, none, nullptr))
       return false;
-    M.jit = jitCached(S, device);
+    M.jit = jitCached(S, device, p.knobs.jitDepth);
     if (!M.jit)
       return false;
   }
@@ -380,12 +381,27 @@ int planStep(hg_plan &p, cudaStream_t st) {
     L.chunks = p.chunks;
     L.geo = p.starGeo;
     L.zorder_boundary_last = p.boundaryLast;
+    L.order = &p.order;
     L.wait_flags = p.waitFlags;
     L.wait_epoch = p.waitEpoch;
     L.wait_mask = p.waitMask;
+    L.err = p.waitErr;
+    L.timeout_ns = p.waitTimeout;
+    L.cur = p.dptr[static_cast<size_t>(bCur)];
+    for (int sd = 0; sd < 2; ++sd) {
+      L.xin[sd] = p.xin[sd];
+      L.xw[sd] = p.xw[sd];
+    }
+    L.split_event = p.splitEvent;
+    L.split_mask = p.splitMask;
     p.waitFlags = nullptr;
+    p.waitErr = nullptr;
+    p.xin[0] = p.xin[1] = nullptr;
+    p.splitEvent = nullptr;
+    p.splitMask = 0;
     if (p.fuse.fuse) {
       L.fuse = 1;
+      L.xpack = p.fuse.xpack;
       for (int d = 0; d < 6; ++d) {
         L.hs[d] = p.fuse.hs[d];
         L.peer[d] = p.fuse.peer[d];
@@ -487,12 +503,13 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
     p->applies.assign(prog->applies, prog->applies + prog->napplies);
     p->prog.applies = p->applies.data();
   }
-  int st = analyze(p->prog, p->an);
+  p->knobs = readKnobs();
+  int st = analyze(p->prog, p->an, !p->knobs.noStar);
   if (st)
     return st;
   // a multi-apply step runs as one fused single-apply program when its temps inline within
   // the op budget (hg_fuse_applies); else apply by apply through HBM temps
-  if (p->prog.napplies > 0 && !std::getenv("HG_NO_FUSE_APPLIES")) {
+  if (p->prog.napplies > 0 && !p->knobs.noFuseApplies) {
     std::vector<hg_op> fops(HG_MAX_OPS);
     hg_program fused;
     if (hg_fuse_applies(&p->prog, &fused, fops.data(), HG_MAX_OPS) == HG_OK) {
@@ -502,7 +519,7 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
       p->prog = fused;
       p->prog.ops = p->ops.data();
       p->applies.clear();
-      st = analyze(p->prog, p->an);
+      st = analyze(p->prog, p->an, !p->knobs.noStar);
       if (st)
         return st;
     }
@@ -557,6 +574,11 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
     for (int d = 0; d < g.rank; ++d)
       ext[d] = g.store[0].ub[d] - g.store[0].lb[d];
     p->starGeo = starGeoFor(p->an.star, g.dtype, g.rank, ext);
+    if (p->knobs.starGeo >= 0) // forced tile geometry (tests; heat f32 3D r<=2 only)
+      p->starGeo = g.rank == 3 && g.dtype == HG_F32 && p->an.star.kind == kHeat &&
+                           p->an.star.ntaps <= 2
+                       ? p->knobs.starGeo
+                       : 0;
     p->tmCur.resize(static_cast<size_t>(g.nfields));
     p->tmPrev.resize(static_cast<size_t>(g.nfields));
     for (int f = 0; f < g.nfields; ++f) {
@@ -570,8 +592,8 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
     // any other DAG: the fused-apply family (generated straight-line code) when its tile
     // rims cover the accesses, else the slot-interpreting generic kernel
     std::string why;
-    if (!std::getenv("HG_NO_APPLY_JIT") && jitEligible(g, p->an, &why)) {
-      auto k = jitCached(g, device);
+    if (!p->knobs.noApplyJit && jitEligible(g, p->an, &why)) {
+      auto k = jitCached(g, device, p->knobs.jitDepth);
       if (k) {
         p->jit = k;
         p->an.family = Family::Apply;
@@ -825,10 +847,9 @@ static int copyField(hg_plan *p, int b, void *host, size_t bytes, void *stream, 
   if (st)
     return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  static const char *force = std::getenv("HG_XFER"); // "ce": copy engines only (A/B)
   // downloads: the copy engines' pitched copy already runs at the flat rate (52 GB/s vs 51 for
   // the kernel, tools/xfer_probe.py); uploads: the zero-copy kernel (51 vs 31 GB/s)
-  void *hd = !up || (force && force[0] == 'c') ? nullptr : mappedHost(host);
+  void *hd = !up ? nullptr : mappedHost(host);
   if (hd && reinterpret_cast<uintptr_t>(hd) % 16 == 0) {
     // pinned host memory: one zero-copy pass at the flat PCIe rate (kernels.cu hostXferKernel)
     st = launchHostXfer(p->dptr[static_cast<size_t>(b)], devLayout(L), hd, up ? 1 : 0, skip_lo,
@@ -839,9 +860,7 @@ static int copyField(hg_plan *p, int b, void *host, size_t bytes, void *stream, 
     return st;
   }
   // pageable memory, large fields: through the pinned staging ring
-  static const bool noStage = std::getenv("HG_NO_STAGING") != nullptr; // A/B only
-  if (!noStage && !(force && force[0] == 'c') &&
-      static_cast<size_t>(L.logicalCount()) * L.es >= (size_t(32) << 20) &&
+  if (static_cast<size_t>(L.logicalCount()) * L.es >= (size_t(32) << 20) &&
       !mappedHost(host))
     return stagedCopy(p, b, static_cast<char *>(host), up, s);
   // pageable memory: the copy engines, one pitched copy of the whole field
@@ -916,8 +935,7 @@ namespace hg {
 // (HG_TB=1): bit-exact, but on B200 the FMA-free two-step pass is issue-bound below the
 // HBM-bound single step (profiles/r1_temporal_blocking.md), so it is not the default.
 bool tbEligible(const hg_plan &p) {
-  const char *on = std::getenv("HG_TB");
-  if (!on || on[0] != '1' || p.tbOff || p.an.family != Family::Star || !tbSupported(p.an.star, p.prog.dtype,
+  if (!p.knobs.tb || p.tbOff || p.an.family != Family::Star || !tbSupported(p.an.star, p.prog.dtype,
                                                                    p.prog.rank))
     return false;
   int64_t pts = 1;
@@ -952,7 +970,7 @@ ResLaunch residentLaunchOf(const hg_plan &p) {
 // Small 2D heat plans (both fields fit in the SMs' shared memory) run whole calls in one
 // resident launch; HG_NO_RESIDENT=1 keeps the per-step star kernel (A/B, tests).
 bool residentEligible(const hg_plan &p) {
-  if (std::getenv("HG_NO_RESIDENT") || p.tbOff || p.an.family != Family::Star || p.prog.rank != 2 ||
+  if (p.knobs.noResident || p.tbOff || p.an.family != Family::Star || p.prog.rank != 2 ||
       p.an.star.kind != kHeat || p.prog.nresults != 1 || p.bind.size() != 2)
     return false;
   const ResLaunch L = residentLaunchOf(p);
@@ -1142,7 +1160,7 @@ int hg_plan_run(hg_plan *p, int64_t steps, void *stream) {
   int64_t pts = 1;
   for (int d = 0; d < p->prog.rank; ++d)
     pts *= p->an.dom_ub[d] - p->an.dom_lb[d];
-  const bool noGraph = std::getenv("HG_NO_GRAPH") != nullptr || pts > (int64_t(1) << 22);
+  const bool noGraph = pts > (int64_t(1) << 22);
   if (!noGraph && steps > G && p->graphs.empty()) {
     // one eager step first: per-device kernel attributes are set outside any capture
     st = planStep(*p, s);

@@ -12,6 +12,7 @@
 
 struct hg_plan {
   int device = 0;
+  hg::Knobs knobs;                    // family selectors, read once at creation
   hg_program prog{};
   std::vector<hg_op> ops;
   hg::Analysis an;
@@ -32,6 +33,16 @@ struct hg_plan {
   unsigned long long waitEpoch = 0;
   int waitMask = 0;
   hg::StarLaunch fuse{};              // one-shot: fused-swap fields (fuse.fuse != 0)
+  // one-shot dmp extras of the next star launch: bounded-wait error word + timeout, packed
+  // x-face receive slabs of the cur buffer, and (NCCL transport) an event the halo-reading
+  // units wait for while the interior units run
+  unsigned long long *waitErr = nullptr;
+  unsigned long long waitTimeout = 0;
+  const void *xin[2] = {nullptr, nullptr};
+  int xw[2] = {0, 0};
+  cudaEvent_t splitEvent = nullptr;
+  int splitMask = 0;
+  hg::UnitOrderCache order;           // star launch orders (boundary units last)
   std::shared_ptr<hg::JitKernel> jit;  // fused-apply family (generated, per program)
   std::vector<CUtensorMap> tmApply;   // per buffer, for the fused-apply boxes
   std::map<int, cudaGraphExec_t> graphs; // hg_plan_run: captured G-step graphs per phase

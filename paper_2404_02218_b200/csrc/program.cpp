@@ -426,7 +426,27 @@ time_slots : {
   return HG_OK;
 }
 
-int analyze(const hg_program &p, Analysis &a) {
+Knobs readKnobs() {
+  auto on = [](const char *n) {
+    const char *e = std::getenv(n);
+    return e && e[0] && e[0] != '0';
+  };
+  auto num = [](const char *n, int dflt) {
+    const char *e = std::getenv(n);
+    return e && e[0] ? std::atoi(e) : dflt;
+  };
+  Knobs k;
+  k.noStar = on("HG_NO_STAR");
+  k.noApplyJit = on("HG_NO_APPLY_JIT");
+  k.noFuseApplies = on("HG_NO_FUSE_APPLIES");
+  k.noResident = on("HG_NO_RESIDENT");
+  k.tb = on("HG_TB");
+  k.starGeo = num("HG_STAR_GEO", -1);
+  k.jitDepth = std::max(0, num("HG_JIT_DEPTH", 0));
+  return k;
+}
+
+int analyze(const hg_program &p, Analysis &a, bool allowStar) {
   int st = validateProgram(p);
   if (st)
     return st;
@@ -512,7 +532,7 @@ int analyze(const hg_program &p, Analysis &a) {
     if (!boundsEqual(p.fields[f], p.fields[0], p.rank))
       sameBounds = false;
   // HG_NO_STAR (tests only) routes star programs through the fused-apply family
-  if (p.rank >= 2 && sameBounds && !std::getenv("HG_NO_STAR") && Matcher(p).match(s)) {
+  if (p.rank >= 2 && sameBounds && allowStar && Matcher(p).match(s)) {
     a.family = Family::Star;
     a.star = s;
     static const char *kinds[] = {"heat", "wave", "copy"};

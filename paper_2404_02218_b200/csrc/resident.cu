@@ -348,15 +348,8 @@ bool geometry(const ResLaunch &L, ResGeometry &g) {
     g.PL += 4;
   g.SP = (g.PL + W + 8 + 3) / 4 * 4;
   const size_t cap = 227 * 1024;
-  static const int kMax = [] { // tuning experiments only
-    const char *e = std::getenv("HG_RES_K"); // default 2: best of 1/2/4/6/8 (r1_sweeps.md)
-    return e ? std::max(1, std::atoi(e)) : 2;
-  }();
-  static const int gMax = [] { // tuning experiments only
-    const char *e = std::getenv("HG_RES_G");
-    return e ? std::max(1, std::atoi(e)) : 1 << 30;
-  }();
-  for (int G = std::min(std::min(numSMs(), gMax), ny); G >= 1; --G) {
+  constexpr int kMax = 2; // steps per exchange: best of 1/2/4/6/8 (r1_sweeps.md)
+  for (int G = std::min(numSMs(), ny); G >= 1; --G) {
     const int minRows = ny / G, maxRows = (ny + G - 1) / G;
     int K = std::min(kMax, minRows / R); // steps per exchange
     if (K < 1)

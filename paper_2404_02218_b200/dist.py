@@ -1,6 +1,7 @@
 """Multi-rank plumbing: one process per GPU, torch.distributed only for the host-side
-handshake (CUDA IPC handle exchange, barriers, max-over-ranks timing).  The halo data itself
-moves GPU-to-GPU over NVLink through the dmp put kernels (hg_dmp_run)."""
+handshake (CUDA IPC handle / NCCL id exchange, barriers, max-over-ranks timing).  The halo data
+itself moves GPU-to-GPU inside the library (hg_dmp_run): NVLink peer stores fused into the
+stencil kernel (transport "p2p"), or NCCL send/recv driven from C++ (transport "nccl")."""
 from __future__ import annotations
 
 from typing import List, Sequence
@@ -27,7 +28,8 @@ def weak_grid(world: int, ndim: int = 3) -> List[int]:
 
 
 def strong_grid(world: int) -> List[int]:
-    """Near-cubic process grids for a fixed global domain (1, 2x1x1, 2x2x1, 2x2x2)."""
+    """Near-cubic process grids for a fixed global domain (1, 2x1x1, 2x2x1, 2x2x2); the x
+    faces of 2x2x2 travel as packed slabs on the fused path."""
     table = {1: [1, 1, 1], 2: [2, 1, 1], 4: [2, 2, 1], 8: [2, 2, 2]}
     if world in table:
         return table[world]
@@ -51,65 +53,18 @@ def origin_of(rank: int, grid: Sequence[int], core: Sequence[int]) -> List[int]:
     return [c[d] * core[d] for d in range(len(grid))]
 
 
-class NcclSwap:
-    """The comparison transport (SURVEY §8 e): every dmp.swap of a step as packed boxes moved
-    by NCCL point-to-point (torch.distributed batch_isend_irecv), then unpacked -- the
-    reference's RankHooks::swap (simulator.cpp:772-834) with NCCL as the Transport.  The
-    product path is hg_dmp_run (the stencil kernel stores the next step's send boxes straight
-    into the neighbours' halos over NVLink); this class exists to measure against it.
+def make_dmp(plan, decomp, rank: int, grid: Sequence[int], world: int, transport: str = "p2p",
+             timeout_s: float = 0.0, group=None):
+    """This rank's hg_dmp on the chosen transport, connected: P2P ranks exchange CUDA IPC
+    blobs with their face neighbours; NCCL ranks share one ncclUniqueId (rank 0's)."""
+    import torch.distributed as dist
 
-    One step = for each swap in program order: pack every send box (hg_plan_pack), one NCCL
-    group of sends/receives with the face neighbours, unpack into the halo boxes; then the
-    stencil step (hg_plan_run(1)).  Same stream throughout; NCCL waits on it and it waits on
-    NCCL (work.wait())."""
-
-    def __init__(self, plan, decomp, rank: int, grid: Sequence[int], stream=None):
-        import numpy as np
-        import torch
-        self.plan, self.rank, self.stream = plan, rank, stream
-        n = decomp.ndim
-        self.dtype = torch.float32 if plan.program.dtype == np.float32 else torch.float64
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.swaps = []
-        for s in range(decomp.nswaps):
-            sw = decomp.swaps[s]
-            jobs = []
-            for k in range(sw.nexchanges):
-                e = sw.ex[k]
-                to = list(e.to[:n])
-                nb = neighbor_rank(rank, to, grid)
-                if nb < 0:
-                    continue
-                size = list(e.size[:n])
-                cnt = 1
-                for x in size:
-                    cnt *= x
-                src_at = [e.at[d] + e.offset[d] for d in range(n)]
-                jobs.append((nb, src_at, list(e.at[:n]), size,
-                             torch.empty(cnt, dtype=self.dtype, device=dev),
-                             torch.empty(cnt, dtype=self.dtype, device=dev)))
-            self.swaps.append((sw.field, jobs))
-        self.bytes = 0
-
-    def step(self):
-        import torch.distributed as dist
-        perm, _ = self.plan.binding()
-        for field, jobs in self.swaps:
-            if not jobs:
-                continue
-            b = perm[field]
-            ops = []
-            for nb, src_at, dst_at, size, sbuf, rbuf in jobs:
-                self.plan.pack(b, src_at, size, sbuf.data_ptr(), self.stream)
-                ops.append(dist.P2POp(dist.isend, sbuf, nb))
-                ops.append(dist.P2POp(dist.irecv, rbuf, nb))
-                self.bytes += sbuf.numel() * sbuf.element_size()
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-            for nb, src_at, dst_at, size, sbuf, rbuf in jobs:
-                self.plan.unpack(b, dst_at, size, rbuf.data_ptr(), self.stream)
-        self.plan.run(1, stream=self.stream)
-
-    def run(self, steps: int):
-        for _ in range(steps):
-            self.step()
+    from . import Dmp, nccl_unique_id
+    if transport == "nccl":
+        box = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        return Dmp(plan, decomp, rank, transport="nccl", nccl_id=box[0], nranks=world,
+                   timeout_s=timeout_s)
+    dmp = Dmp(plan, decomp, rank, timeout_s=timeout_s)
+    connect(dmp, rank, grid, world, group=group)
+    return dmp

@@ -59,11 +59,12 @@ def test_ipc_dmp_two_ranks(args):
      "--calls", "1,3"],
 ])
 def test_nccl_transport_baseline(args):
-    # the NCCL comparison transport (dist.NcclSwap) is bit-exact too, halos included
+    # the NCCL transport (C++: pack, ncclSend/ncclRecv on a side stream, unpack, interior
+    # units overlapped) is bit-exact too, halos included
     n = _ngpus()
     if n < 2:
         pytest.skip("needs 2 GPUs")
-    for nproc, grid in ((2, "2x1x1"), (4, "2x2x1")):
+    for nproc, grid in ((2, "2x1x1"), (2, "1x1x2"), (4, "2x2x1"), (4, "1x2x2")):
         if nproc > n:
             continue
         cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone",
@@ -161,3 +162,71 @@ def test_ipc_dmp_multi_chunk(kind, order, extents, grid, T, calls):
     r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,rank,order,extents,grid,T,calls,extra", [
+    # grids that split the contiguous last dim: x faces travel as packed slabs [y][z][w],
+    # sent by the producing CTAs in 16-byte stores and unpacked by the receiving CTAs' producer
+    # warp before their TMA loads (and by the stand-alone put on a call's first step)
+    ("heat", 3, 4, "256x128x512", "1x1x2", 5, "1,4", []),
+    ("heat", 3, 4, "200x800x1600", "1x1x2", 3, None, []),          # wide 128x12 tile
+    ("wave", 3, 8, "400x48x192", "1x1x2", 4, "2,2", []),
+    ("heat", 3, 8, "120x40x250", "1x1x2", 3, None, []),            # ragged, 125 = odd width
+    ("heat", 2, 2, "256x512", "1x2", 6, "3,3", []),
+    ("heat", 3, 4, "256x128x512", "1x1x2", 4, "2,2", ["--upload"]),
+    ("heat", 3, 4, "192x256x256", "1x2x2", 4, None, []),
+    ("heat", 3, 4, "256x256x256", "2x1x2", 3, "1,2", []),
+    ("wave", 3, 8, "200x96x200", "1x1x4", 3, None, []),
+])
+def test_ipc_dmp_x_faces(kind, rank, order, extents, grid, T, calls, extra):
+    n = _ngpus()
+    nproc = int(np.prod([int(x) for x in grid.split("x")]))
+    if n < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node",
+           str(nproc), os.path.join(REPO, "tools", "dmp_check.py"), "--kind", kind, "--rank",
+           str(rank), "--order", str(order), "--extents", extents, "--grid", grid, "--T",
+           str(T)] + extra
+    if calls:
+        cmd += ["--calls", calls]
+    r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec,grid,T", [
+    (("heat", 3, 48, 4), [2, 1, 1], 5), (("heat", 3, 48, 4), [1, 1, 2], 5),
+    (("wave", 3, 40, 8), [1, 2, 1], 4), (("heat", 2, 64, 2), [1, 2], 6),
+    (("heat", 3, 64, 4), [2, 2, 1], 4), (("heat", 3, 64, 4), [1, 2, 2], 3),
+])
+def test_simulate_one_rank_per_device(port, spec, grid, T):
+    # hg_sim_run with one rank per GPU takes the multi-process protocol (fused NVLink swap,
+    # in-kernel flag waits, packed x faces) from one host thread: gathered result == serial
+    import paper_2404_02218_b200 as hg
+    n = _ngpus()
+    nr = int(np.prod(grid))
+    if n < nr:
+        pytest.skip(f"needs {nr} GPUs")
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    init = hg.initial_fields(prog)
+    out = hg.simulate(prog, grid, init, T, devices=list(range(nr)))
+    arrays = [b.data.copy() for b in init]
+    perm = port.run(prog, arrays, T)
+    for b, p in zip(out, perm):
+        assert np.array_equal(b.data.view(np.uint32), arrays[p].view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_stuck_peer_reports_instead_of_hanging():
+    # a neighbour that never runs: rank 0's halo wait times out and surfaces as HG_ETRAP
+    # ("... did not arrive for epoch e within 2.0 s ...") instead of a hung GPU
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "2",
+           os.path.join(REPO, "tools", "stuck_peer.py")]
+    r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "STUCK-PEER REPORTED" in r.stdout, r.stdout[-3000:]

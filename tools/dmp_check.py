@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--T", type=int, default=5)
     ap.add_argument("--calls", default=None, help="split T over several run calls, e.g. 2,3")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="p2p: hg_dmp (fused NVLink puts); nccl: the packed-box NCCL baseline")
+                    help="p2p: fused NVLink puts; nccl: packed boxes over NCCL (C++ transport)")
     ap.add_argument("--upload", action="store_true",
                     help="the e2e path of bench.py: fields from pinned host buffers via "
                          "hg_plan_upload_live over poisoned device buffers")
@@ -39,10 +39,7 @@ def main():
     rank = int(os.environ["RANK"])
     lr = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr)
-    if a.transport == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
-    else:
-        dist.init_process_group("gloo")
+    dist.init_process_group("gloo")
     grid = [int(x) for x in a.grid.split("x")] if a.grid else [world] + [1] * (a.rank - 1)
     if a.golden:
         import json
@@ -60,11 +57,7 @@ def main():
     coord = hg.coord_from_rank(rank, grid)
     plan.init_fields(origin=[coord[d] * dc.core[d] for d in range(a.rank)])
     from paper_2404_02218_b200 import dist as hd
-    if a.transport == "nccl":
-        dmp = hd.NcclSwap(plan, dc, rank, grid)
-    else:
-        dmp = hg.Dmp(plan, dc, rank)
-        hd.connect(dmp, rank, grid, world)
+    dmp = hd.make_dmp(plan, dc, rank, grid, world, transport=a.transport)
     dist.barrier()
     if a.upload:
         host = [torch.from_numpy(plan.download(i)).pin_memory().numpy()
@@ -74,14 +67,12 @@ def main():
         plan.reset_binding()
         for i in range(local.nfields):
             plan.upload(i, host[i], live=True)
-        if a.transport != "nccl":
-            dmp.invalidate()
-        torch.cuda.synchronize()
-        dist.barrier()
+        dmp.invalidate()  # collective: the next run starts with the receiver-ready handshake
     calls = [int(x) for x in a.calls.split(",")] if a.calls else [a.T]
     assert sum(calls) == a.T
     for c in calls:
         dmp.run(c)
+    dmp.status()
     torch.cuda.synchronize()
     perm, _ = plan.binding()
     got = [plan.download(p) for p in perm]
@@ -91,16 +82,14 @@ def main():
     lbs = [prog.field_bounds(i)[0] for i in range(prog.nfields)]
     want = port.simulate_rank_state(local, dc, glob, lbs, a.T, rank)
     ok = all(np.array_equal(g.view(np.uint8), w.view(np.uint8)) for g, w in zip(got, want))
-    flag = torch.tensor([0 if ok else 1], device="cuda" if a.transport == "nccl" else "cpu")
+    flag = torch.tensor([0 if ok else 1])
     dist.all_reduce(flag)
     dist.barrier()
-    if a.transport != "nccl":
-        dmp.close()
+    dmp.close()
     plan.close()
     if rank == 0:
-        print(f"dmp_check {a.kind}{a.rank}d n{a.extent} o{a.order} grid={grid} T={a.T}: "
-              f"{'OK' if flag.item() == 0 else 'MISMATCH'} (bytes put by rank0 "
-              f"{dmp.bytes_exchanged() if False else 'n/a'})", flush=True)
+        print(f"dmp_check {a.kind}{a.rank}d n{a.extent} o{a.order} grid={grid} T={a.T} "
+              f"transport={a.transport}: {'OK' if flag.item() == 0 else 'MISMATCH'}", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 0 else 1)
 
