@@ -354,7 +354,7 @@ def run_ours(args):
     wl = WORKLOADS[args.workload]
     if wl["kind"] == "heat3d":
         glob = hg.build_kernel(hg.KernelSpec("heat", 3, E, 4, "f32")).with_extents(gext)
-        local, dc = glob.decompose(grid)
+        local, dc = glob.decompose(grid, depth=args.depth if world > 1 else 1)
         origin = hd.origin_of(rank, grid, list(dc.core[:3]))
     else:  # single-GPU BASELINE configs; N > 1 runs independent replicas
         grid = [1] * 3
@@ -368,7 +368,7 @@ def run_ours(args):
         # packed slabs there, so no grid needs the NCCL transport
         transport = "p2p"
     if world > 1 and dc is not None:
-        dmp = hd.make_dmp(plan, dc, rank, grid, world, transport=transport)
+        dmp = hd.make_dmp(plan, dc, rank, grid, world, transport=transport, depth=args.depth)
         dist.barrier()
 
     def steps(k):
@@ -508,7 +508,7 @@ def run_ours(args):
                        "kernel": plan.kernel_name,
                        "core_per_gpu": list(dc.core[:3]) if dc is not None else None,
                        "global_core": gext if dc is not None else core_extents(local),
-                       "grid": grid, "halo": halo_width(local),
+                       "grid": grid, "halo": halo_width(local), "halo_depth": args.depth,
                        "l2": ("8.4 MB of fields < 126 MB L2; by design they stay on chip "
                               "(shared memory) for a whole run call, so no flush applies"
                               if args.workload == "heat2d_1024" else
@@ -553,6 +553,8 @@ def main():
                     help="halo transport at N>1: p2p = fused NVLink stores from the stencil "
                          "kernel, nccl = packed boxes over NCCL send/recv on a side stream "
                          "(C++), auto = p2p")
+    ap.add_argument("--depth", type=int, default=1,
+                    help="deep halos at N>1: exchange depth*h-wide halos every `depth` steps")
     ap.add_argument("--workload", default="heat3d_weak", choices=list(WORKLOADS))
     ap.add_argument("--strong-extent", type=int, default=2048)
     ap.add_argument("--e2e-timesteps", type=int, default=100)

@@ -234,6 +234,12 @@ int hg_apply_compile(const hg_program *prog, char *src, size_t cap, size_t *cubi
  * applies with their domains rewritten to the local core. */
 int hg_decompose_program(const hg_program *global, int ndim, const int64_t *grid,
                          hg_program *local, hg_decomp *decomp);
+/* The same, with halos (and exchange boxes) `depth` times as wide in every split dimension
+ * (grid > 1): the communication-avoiding form hg_dmp runs with hg_dmp_opts.depth = depth.
+ * Beyond the reference (which swaps before every load, dmp_transforms.cpp:276-300); the
+ * gathered cores stay bit-identical. */
+int hg_decompose_program_deep(const hg_program *global, int ndim, const int64_t *grid,
+                              int depth, hg_program *local, hg_decomp *decomp);
 
 /* ---- plans: device-resident fields + the compiled step --------------------------------- */
 int hg_plan_create(const hg_program *prog, int device, hg_plan **out);
@@ -284,6 +290,10 @@ typedef struct hg_dmp_opts {
   unsigned char nccl_id[HG_NCCL_ID_BYTES];  /* NCCL: hg_nccl_unique_id() of one rank, shared */
   double timeout_s;                         /* bounded halo waits: 0 = default (30 s),
                                                < 0 = wait forever */
+  int depth;                                /* deep halos: exchange depth*w-wide halos every
+                                               `depth` steps, the ring recomputed redundantly
+                                               (decomposition from hg_decompose_program_deep);
+                                               0 or 1 = every step, as the reference */
 } hg_dmp_opts;
 /* One rank's endpoint of the decomposed program (RankHooks + Endpoint, simulator.cpp:201-260,
  * 772-834).  hg_dmp_create = hg_dmp_create_ex with default options (P2P). */

@@ -291,16 +291,22 @@ class Program:
         check(lib().hg_program_match(C.byref(self.prog), buf, 128))
         return buf.value.decode()
 
-    def decompose(self, grid: Sequence[int]):
-        """The decompose pass: returns (local program, HgDecomp)."""
+    def decompose(self, grid: Sequence[int], depth: int = 1):
+        """The decompose pass: returns (local program, HgDecomp).  depth > 1: halos and
+        exchange boxes depth x as wide in the split dims (hg_decompose_program_deep), for a
+        Dmp(..., depth=depth) that exchanges every `depth` steps."""
         local = HgProgram()
         dc = HgDecomp()
         aps = None
         if self.prog.napplies > 0:
             aps = (capi.HgApply * self.prog.napplies)()
             local.applies = C.cast(aps, C.POINTER(capi.HgApply))
-        check(lib().hg_decompose_program(C.byref(self.prog), len(grid), _i64(grid),
-                                         C.byref(local), C.byref(dc)))
+        if depth > 1:
+            check(lib().hg_decompose_program_deep(C.byref(self.prog), len(grid), _i64(grid),
+                                                  depth, C.byref(local), C.byref(dc)))
+        else:
+            check(lib().hg_decompose_program(C.byref(self.prog), len(grid), _i64(grid),
+                                             C.byref(local), C.byref(dc)))
         out = Program(local, self.ops)
         if aps is not None:
             out.applies = aps
@@ -463,13 +469,15 @@ class Dmp:
     library default, < 0: forever)."""
 
     def __init__(self, plan: Plan, decomp: HgDecomp, rank: int, transport: str = "p2p",
-                 nccl_id: Optional[bytes] = None, nranks: int = 0, timeout_s: float = 0.0):
+                 nccl_id: Optional[bytes] = None, nranks: int = 0, timeout_s: float = 0.0,
+                 depth: int = 1):
         self.plan = plan
         h = C.c_void_p()
         o = capi.HgDmpOpts()
         o.transport = capi.HG_TRANSPORT_NCCL if transport == "nccl" else capi.HG_TRANSPORT_P2P
         o.nranks = nranks
         o.timeout_s = timeout_s
+        o.depth = depth
         if nccl_id is not None:
             C.memmove(o.nccl_id, nccl_id, capi.HG_NCCL_ID_BYTES)
         check(lib().hg_dmp_create_ex(plan.h, C.byref(decomp), rank, C.byref(o), C.byref(h)))
@@ -519,13 +527,14 @@ def nccl_unique_id() -> bytes:
 
 
 def simulate(prog: Program, grid: Sequence[int], global_init: List[Buffer], timesteps: int,
-             devices: Optional[Sequence[int]] = None) -> List[Buffer]:
+             devices: Optional[Sequence[int]] = None, depth: int = 1) -> List[Buffer]:
     """exec::simulate (simulator.cpp:1066-1203): decompose, scatter, run every rank on the
     GPU(s) of this process with device halo swaps, gather the cores.
 
     Result i = global field bound to slot i at the end, gathered over a copy of the initial
-    global buffer of that slot's origin (so the global-boundary ring is the initial one)."""
-    local, dc = prog.decompose(grid)
+    global buffer of that slot's origin (so the global-boundary ring is the initial one).
+    depth > 1: deep halos (exchange every `depth` steps, needs one rank per device)."""
+    local, dc = prog.decompose(grid, depth=depth)
     nranks = int(np.prod(grid))
     ndev = lib_device_count()
     devs = list(devices) if devices is not None else [r % max(ndev, 1) for r in range(nranks)]
@@ -537,12 +546,21 @@ def simulate(prog: Program, grid: Sequence[int], global_init: List[Buffer], time
             for f in range(prog.nfields):
                 g = global_init[f]
                 llo, lhi = local.field_bounds(f)
-                sl = tuple(slice(llo[d] + coord[d] * dc.core[d] - g.lb[d],
-                                 lhi[d] + coord[d] * dc.core[d] - g.lb[d])
-                           for d in range(prog.rank))
-                pl.upload(f, g.data[sl])           # scatterRank (simulator.cpp:995-1025)
+                lo = [llo[d] + coord[d] * dc.core[d] - g.lb[d] for d in range(prog.rank)]
+                hi = [lhi[d] + coord[d] * dc.core[d] - g.lb[d] for d in range(prog.rank)]
+                if all(lo[d] >= 0 and hi[d] <= g.data.shape[d] for d in range(prog.rank)):
+                    sl = tuple(slice(lo[d], hi[d]) for d in range(prog.rank))
+                    pl.upload(f, g.data[sl])       # scatterRank (simulator.cpp:995-1025)
+                else:  # deep halos reach past the global ring: those cells are never read
+                    a = np.zeros([hi[d] - lo[d] for d in range(prog.rank)], dtype=g.data.dtype)
+                    src = tuple(slice(max(lo[d], 0), min(hi[d], g.data.shape[d]))
+                                for d in range(prog.rank))
+                    dst = tuple(slice(max(lo[d], 0) - lo[d], min(hi[d], g.data.shape[d]) - lo[d])
+                                for d in range(prog.rank))
+                    a[dst] = g.data[src]
+                    pl.upload(f, a)
             plans.append(pl)
-            dmps.append(Dmp(pl, dc, r))
+            dmps.append(Dmp(pl, dc, r, depth=depth))
         arr = (C.c_void_p * nranks)(*[d.h for d in dmps])
         check(lib().hg_sim_connect(arr, nranks))
         check(lib().hg_sim_run(arr, nranks, timesteps, None))

@@ -33,7 +33,8 @@ class HgOp(C.Structure):
 
 class HgDmpOpts(C.Structure):
     _fields_ = [("transport", C.c_int), ("nranks", C.c_int),
-                ("nccl_id", C.c_ubyte * HG_NCCL_ID_BYTES), ("timeout_s", C.c_double)]
+                ("nccl_id", C.c_ubyte * HG_NCCL_ID_BYTES), ("timeout_s", C.c_double),
+                ("depth", C.c_int)]
 
 
 class HgBounds(C.Structure):
@@ -125,6 +126,8 @@ def lib() -> C.CDLL:
         "hg_fuse_applies": (C.c_int, [P(HgProgram), P(HgProgram), P(HgOp), C.c_int]),
         "hg_parse_program": (C.c_int, [C.c_char_p, P(HgProgram), P(HgOp), C.c_int, P(HgApply),
                                        C.c_int, P(HgDecomp), P(C.c_int), C.c_char_p, SZ]),
+        "hg_decompose_program_deep": (C.c_int, [P(HgProgram), C.c_int, P(I64), C.c_int,
+                                                P(HgProgram), P(HgDecomp)]),
         "hg_decompose_program": (C.c_int, [P(HgProgram), C.c_int, P(I64), P(HgProgram),
                                            P(HgDecomp)]),
         "hg_plan_create": (C.c_int, [P(HgProgram), C.c_int, P(V)]),

@@ -158,6 +158,12 @@ struct hg_dmp {
   unsigned long long timeoutNs = 0;
   bool prof = false;
   NcclState nc;
+  // deep halos (communication-avoiding): exchange depth*w-wide halos every `depth` steps;
+  // step j of a round of klen steps computes the core extended by (klen-1-j)*unit[dim] toward
+  // every neighbour (the same DAG on the same inputs as the neighbour's, so bit-identical)
+  int depth = 1;
+  int64_t unit[HG_MAX_RANK] = {0, 0, 0};
+  int phase = 0, klen = 1;
 };
 
 namespace hg {
@@ -337,8 +343,23 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     evs->push_back(e);
   };
   unsigned long long *err = d.flags + kErr;
+  const int r = g.rank;
+  if (d.depth > 1) {
+    if (t == 0) { // a call starts a round: every swapped field goes out at full depth width
+      d.phase = 0;
+      std::fill(d.dirty.begin(), d.dirty.end(), 1);
+    }
+    if (d.phase == 0)
+      d.klen = static_cast<int>(std::min<int64_t>(d.depth, steps - t));
+  }
+  const int ph = d.depth > 1 ? d.phase : 0, kl = d.depth > 1 ? d.klen : 1;
+  int64_t ext[HG_MAX_RANK][2] = {{0, 0}, {0, 0}, {0, 0}};
+  for (int di = 0; di < 2 * r; ++di)
+    if (d.nbr[di] >= 0)
+      ext[di / 2][di & 1] = (kl - 1 - ph) * d.unit[di / 2];
   // 0. receiver-ready handshake after host uploads (hg_dmp_invalidate is collective): no
   //    neighbour may put into my buffers before my uploads into them are done
+  const bool handshake = d.needReady;
   if (d.needReady) {
     ++d.readyEpoch;
     unsigned long long *pr[kDirs] = {};
@@ -354,9 +375,19 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     d.needReady = false;
   }
   const bool star = starPlan(p);
-  // 1. stand-alone put of every dirty swapped buffer
+  // deep halos: the call's first put rewrites halos the neighbours read in the last step of
+  // their previous call (e.g. wave's prev band), so it waits for the signal round that step
+  // published (after a ready handshake everybody's earlier work is done anyway)
+  if (d.depth > 1 && t == 0 && d.epoch > 0 && !handshake && nw) {
+    if (int rc = launchWaitFlags(d.flags, widx, nw, d.epoch, err, d.timeoutNs, st))
+      return rc;
+    ++p.launches;
+  }
+  // 1. stand-alone put of every dirty swapped buffer, straight into the neighbours' halos
+  //    (x faces too: only rounds a fused put produced arrive as packed slabs)
+  const bool packedRound = d.roundReady;
   std::vector<PutJob> jobs;
-  if (int rc = buildPutJobs(d, jobs, d.xpack))
+  if (int rc = buildPutJobs(d, jobs, false))
     return rc;
   mark();
   if (!d.roundReady || !jobs.empty()) {
@@ -374,7 +405,11 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     p.waitMask = mask;
     p.waitErr = err;
     p.waitTimeout = d.timeoutNs;
-    if (d.xpack) { // the cur buffer's x halo arrives packed
+    for (int q = 0; q < r; ++q) {
+      p.regionExt[q][0] = ext[q][0];
+      p.regionExt[q][1] = ext[q][1];
+    }
+    if (d.xpack && ph == 0 && packedRound) { // the cur buffer's x halo arrives packed
       const int xd = g.rank - 1;
       const int bCur =
           p.bind[static_cast<size_t>(g.operand_field[p.an.star.cur_operand])];
@@ -394,6 +429,16 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
           p.xin[sd] = d.slab + slabOffset(d, bCur, sd);
           p.xw[sd] = w;
         }
+      }
+      if (d.depth > 1) { // the receive box relative to the (extended) region
+        const hg_bounds &sb = g.store[0];
+        p.xboxSet = true;
+        p.xbox[0] = static_cast<int>(ext[0][0]);
+        p.xbox[1] = r == 3 ? static_cast<int>(ext[1][0]) : 0;
+        p.xbox[2] = static_cast<int>(sb.ub[0] - sb.lb[0]);
+        p.xbox[3] = r == 3 ? static_cast<int>(sb.ub[1] - sb.lb[1]) : 1;
+        p.xbox[4] = static_cast<int>(ext[xd][0]) - p.xw[0];
+        p.xbox[5] = static_cast<int>(ext[xd][0] + sb.ub[xd] - sb.lb[xd]);
       }
     }
   } else if (nw) {
@@ -416,7 +461,25 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     if (d.dc.swaps[k].field == nextSlot)
       sw = &d.dc.swaps[k];
   bool fused = false;
-  if (star && nw && sw && t + 1 < steps) {
+  bool signalOnly = false;
+  if (star && nw && (ph < kl - 1 || (d.depth > 1 && t + 1 == steps))) {
+    // a step inside a deep round (or the last step of a deep call): no payload, but its
+    // halo-reading units signal the neighbours when done (who may then overwrite those halos
+    // in the round's last step, or in the first put of the next call)
+    StarLaunch F{};
+    for (int di = 0; di < 2 * r; ++di)
+      if (d.nbr[di] >= 0) {
+        F.hs[di] = 1;
+        F.nodata |= 1 << di;
+        F.peer_flag[di] = d.peerFlags[di];
+      }
+    F.fuse = 1;
+    F.cnt = d.cnt6;
+    F.cnt_accum = d.cntAccum;
+    F.put_epoch = d.epoch + 1;
+    p.fuse = F;
+    fused = signalOnly = true;
+  } else if (star && nw && sw && t + 1 < steps) {
     StarLaunch F{};
     const Layout &L = p.lay[static_cast<size_t>(bOut)];
     const int r = g.rank;
@@ -481,6 +544,9 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
       p.fuse = F;
       d.bytes += payload;
       fused = true;
+    } else if (d.depth > 1) {
+      return setError(HG_EUNSUPPORTED, "deep halos need the fused swap (exchange boxes that "
+                                       "are bands of the core)");
     }
   }
   mark();
@@ -489,22 +555,39 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
   mark();
   for (size_t k = 1; k < written.size(); ++k) // (multi-store programs never fuse)
     d.dirty[static_cast<size_t>(written[k])] = 1;
-  d.dirty[static_cast<size_t>(bOut)] = fused ? 0 : 1;
+  d.dirty[static_cast<size_t>(bOut)] = fused && !signalOnly ? 0 : 1;
   if (fused)
     ++d.epoch;
   d.roundReady = fused;
+  if (d.depth > 1)
+    d.phase = (ph + 1) % kl;
   return HG_OK;
 }
 
 // One time step on the NCCL transport: pack the dirty send boxes on the compute stream, NCCL
 // send/recv + unpack on the comm stream, the stencil's interior units meanwhile, then the
 // units that read the halos (star plans; other families wait for the halos first).
-int ncclStep(hg_dmp &d, cudaStream_t st) {
+int ncclStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st) {
   hg_plan &p = *d.plan;
   NcclApi &api = nccl();
+  const int r0 = p.prog.rank;
+  if (d.depth > 1) {
+    if (t == 0) {
+      d.phase = 0;
+      std::fill(d.dirty.begin(), d.dirty.end(), 1);
+    }
+    if (d.phase == 0)
+      d.klen = static_cast<int>(std::min<int64_t>(d.depth, steps - t));
+  }
+  const int ph = d.depth > 1 ? d.phase : 0, kl = d.depth > 1 ? d.klen : 1;
+  if (d.depth > 1)
+    for (int di = 0; di < 2 * r0; ++di)
+      if (d.nbr[di] >= 0)
+        p.regionExt[di / 2][di & 1] = (kl - 1 - ph) * d.unit[di / 2];
   std::vector<Xjob> xs;
-  if (int rc = collectJobs(d, xs))
-    return rc;
+  if (ph == 0) // deep halos: one exchange per round
+    if (int rc = collectJobs(d, xs))
+      return rc;
   int mask = 0;
   for (int di = 0; di < kDirs; ++di)
     if (d.nbr[di] >= 0)
@@ -594,6 +677,8 @@ int ncclStep(hg_dmp &d, cudaStream_t st) {
     return rc;
   for (int b : written)
     d.dirty[static_cast<size_t>(b)] = 1;
+  if (d.depth > 1)
+    d.phase = (ph + 1) % kl;
   return HG_OK;
 }
 
@@ -712,6 +797,33 @@ int hg_dmp_create_ex(hg_plan *plan, const hg_decomp *dc, int64_t rank, const hg_
     d->dirty.assign(plan->dptr.size(), 1);
     d->xpack = o.transport == HG_TRANSPORT_P2P && starPlan(*plan) && plan->prog.rank >= 2 &&
                slabElems > 0;
+    d->depth = o.depth < 1 ? 1 : o.depth;
+    if (d->depth > 1) {
+      // deep halos: every exchange of a split dim is depth * unit wide, unit >= the stencil
+      // radius (hg_decompose_program_deep builds such programs)
+      if (!starPlan(*plan))
+        return setError(HG_EUNSUPPORTED, "deep halos need a star-family program");
+      // a second-order-in-time step reads prev at the extended points too: prev at a round's
+      // first step is the output of the previous round's second-to-last step, extended by one
+      // width only -- enough for depth 2 alone
+      if (plan->an.star.kind == kWave && d->depth > 2)
+        return setError(HG_EUNSUPPORTED, "deep halos of a prev/cur/next step support depth 2");
+      for (int s = 0; s < dc->nswaps; ++s)
+        for (int k = 0; k < dc->swaps[s].nexchanges; ++k) {
+          const hg_exchange &e = dc->swaps[s].ex[k];
+          for (int q = 0; q < dc->ndim; ++q) {
+            if (e.to[q] == 0 || dc->grid[q] < 2)
+              continue;
+            const int64_t w = e.size[q];
+            if (w % d->depth != 0 || w / d->depth < plan->an.star.radius ||
+                (d->unit[q] && d->unit[q] != w / d->depth))
+              return setError(HG_EINVAL, "deep halos: exchange width " + std::to_string(w) +
+                                             " in dimension " + std::to_string(q) +
+                                             " is not depth x a width >= the stencil radius");
+            d->unit[q] = w / d->depth;
+          }
+        }
+    }
     d->slabElems = d->xpack ? slabElems : 0;
     if (int st = cudaCheck(cudaSetDevice(plan->device), "cudaSetDevice"))
       return st;
@@ -878,7 +990,7 @@ int hg_dmp_run(hg_dmp *d, int64_t steps, void *stream) {
   std::vector<cudaEvent_t> evs;
   d->roundReady = false;
   for (int64_t t = 0; t < steps; ++t) {
-    int rc = d->transport == HG_TRANSPORT_NCCL ? ncclStep(*d, st)
+    int rc = d->transport == HG_TRANSPORT_NCCL ? ncclStep(*d, t, steps, st)
                                                : dmpStep(*d, t, steps, st, d->prof ? &evs : nullptr);
     if (rc)
       return rc;

@@ -151,12 +151,14 @@ template <typename T> struct StarParams {
   T *cur;
   const T *xin[2];
   int xw[2];
+  int xoz, xoy, xbz, xby, xox[2]; // receive box of the slabs, region-relative
   // fused swap of the NEXT step: output points inside a send box (width hs[d] at face d) are
   // also stored into the neighbour's buffer (peer[d] + my index + pdelta[d]), or for a packed
   // x face (xpack bit d) into the neighbour's slab peer[d]; each face's CTAs count completions
   // and the last one publishes put_epoch to the neighbour's flag
   int fuse;
   int xpack;
+  int nodata;    // faces that only signal (deep halos: the rounds between data rounds)
   int hs[6];
   T *peer[6];
   int64_t pdelta[6];
@@ -267,13 +269,13 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
           continue;
         const T *slab = P.xin[sd];
         const int W = P.xw[sd];
-        const int y0 = RANK == 3 ? max(0, yb - RY) : 0;
-        const int y1 = RANK == 3 ? min(P.ny, yb + C::TY + RY) : 1;
-        const int z0 = max(0, zb - R), z1 = min(P.nz, zb + n + R);
+        const int y0 = RANK == 3 ? max(P.xoy, yb - RY) : 0;
+        const int y1 = RANK == 3 ? min(P.xoy + P.xby, yb + C::TY + RY) : 1;
+        const int z0 = max(P.xoz, zb - R), z1 = min(P.xoz + P.xbz, zb + n + R);
         const int per = (z1 - z0) * W;
-        const int64_t xoff = sd ? int64_t(P.nx) : -int64_t(W);
+        const int64_t xoff = P.xox[sd];
         for (int y = y0; y < y1; ++y) {
-          const T *src = slab + (int64_t(y) * P.nz + z0) * W;
+          const T *src = slab + (int64_t(y - P.xoy) * P.xbz + (z0 - P.xoz)) * W;
           T *dst = P.cur + int64_t(P.zs + z0) * P.plane +
                    (RANK == 3 ? int64_t(P.ys + y) * P.pitch : 0) + P.col0 + P.xs + xoff;
           for (int k = plane_lane; k < per; k += 32) {
@@ -554,7 +556,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       const T *src = outRow;
       const int64_t e0 = outRow - P.out;
       for (int d = 0; d < 2 * RANK; ++d) {
-        if (!(blockTouch & (1 << d)) || (P.xpack & (1 << d)))
+        if (!(blockTouch & (1 << d)) || ((P.xpack | P.nodata) & (1 << d)))
           continue;
         const int dim = d >> 1;
         const bool lo = (d & 1) == 0;
@@ -601,7 +603,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         }
       }
     }
-    if (blockTouch & P.xpack) {
+    if (blockTouch & P.xpack & ~P.nodata) {
       // packed x faces: the CTA's rows of the face as slab segments [y][z0..z0+n)[W],
       // contiguous per row, written by all consumer threads in 16-byte stores (each reads the
       // points back from the output rows the CTA just stored; the barrier orders them)
@@ -611,7 +613,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       const int nrows = RANK == 3 ? min(C::TY, P.ny - yb) : 1;
 #pragma unroll 1
       for (int d = 2 * XD; d < 2 * XD + 2; ++d) {
-        if (!(blockTouch & P.xpack & (1 << d)))
+        if (!(blockTouch & P.xpack & ~P.nodata & (1 << d)))
           continue;
         const int W = P.hs[d];
         const int xlo = (d & 1) ? P.nx - W : 0;
@@ -792,6 +794,20 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
     P.xin[sd] = static_cast<const T *>(L.xin[sd]);
     P.xw[sd] = L.xw[sd];
   }
+  if (L.xbox_set) {
+    P.xoz = L.xoz;
+    P.xoy = L.xoy;
+    P.xbz = L.xbz;
+    P.xby = L.xby;
+    P.xox[0] = L.xox[0];
+    P.xox[1] = L.xox[1];
+  } else {
+    P.xoz = P.xoy = 0;
+    P.xbz = P.nz;
+    P.xby = P.ny;
+    P.xox[0] = -L.xw[0];
+    P.xox[1] = P.nx;
+  }
   P.fuse = L.fuse;
   unsigned targets[6] = {0, 0, 0, 0, 0, 0};
   if (L.fuse) {
@@ -807,6 +823,7 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
     };
     const int nyt = RANK == 3 ? P.tiles_y : 1;
     P.xpack = L.xpack;
+    P.nodata = L.nodata;
     for (int d = 0; d < 6; ++d) {
       P.hs[d] = L.hs[d];
       P.peer[d] = static_cast<T *>(L.peer[d]);

@@ -59,9 +59,14 @@ struct StarLaunch {
   void *cur = nullptr;          // base of the buffer bound to the cur operand
   const void *xin[2] = {};      // my receive slabs of that buffer (lo, hi x face), or null
   int xw[2] = {0, 0};           // their widths
+  // receive box of the slabs relative to the output region (deep halos extend the region):
+  // z/y origin and extents, first halo column of the lo/hi face; xbox_set = 0: the region is
+  // the core (origin 0, extents nz/ny, columns -w and nx)
+  int xbox_set = 0, xoz = 0, xoy = 0, xbz = 0, xby = 0, xox[2] = {0, 0};
   // fused swap of the next step (see StarParams in kernels.cu); cnt_accum is host state
   int fuse = 0;
   int xpack = 0;                // bit d: face d is sent packed into the peer's slab peer[d]
+  int nodata = 0;               // bit d: face d only signals (count + publish, no payload)
   int hs[6] = {0, 0, 0, 0, 0, 0};
   void *peer[6] = {};
   int64_t pdelta[6] = {0, 0, 0, 0, 0, 0};

@@ -374,6 +374,21 @@ int planStep(hg_plan &p, cudaStream_t st) {
       L.start[d] = g.store[0].lb[d] - lay.lb[d];
       L.ext[d] = g.store[0].ub[d] - g.store[0].lb[d];
     }
+    for (int d = 0; d < g.rank; ++d) { // deep halos: the region of this step of the round
+      L.start[d] -= p.regionExt[d][0];
+      L.ext[d] += p.regionExt[d][0] + p.regionExt[d][1];
+      p.regionExt[d][0] = p.regionExt[d][1] = 0;
+    }
+    if (p.xboxSet) {
+      L.xbox_set = 1;
+      L.xoz = p.xbox[0];
+      L.xoy = p.xbox[1];
+      L.xbz = p.xbox[2];
+      L.xby = p.xbox[3];
+      L.xox[0] = p.xbox[4];
+      L.xox[1] = p.xbox[5];
+      p.xboxSet = false;
+    }
     L.lay = devLayout(lay);
     L.tm_cur = &p.tmCur[static_cast<size_t>(bCur)];
     L.tm_prev = &p.tmPrev[static_cast<size_t>(bPrev)];
@@ -402,6 +417,7 @@ int planStep(hg_plan &p, cudaStream_t st) {
     if (p.fuse.fuse) {
       L.fuse = 1;
       L.xpack = p.fuse.xpack;
+      L.nodata = p.fuse.nodata;
       for (int d = 0; d < 6; ++d) {
         L.hs[d] = p.fuse.hs[d];
         L.peer[d] = p.fuse.peer[d];

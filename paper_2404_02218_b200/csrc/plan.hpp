@@ -42,6 +42,12 @@ struct hg_plan {
   int xw[2] = {0, 0};
   cudaEvent_t splitEvent = nullptr;
   int splitMask = 0;
+  // deep halos: the step's output region extends past the core by regionExt[d][lo/hi] (the
+  // neighbours' points the next steps of the round need), and the packed x slabs' receive box
+  // relative to that region
+  int64_t regionExt[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  int xbox[6] = {0, 0, 0, 0, 0, 0}; // oz, oy, bz, by, ox_lo, ox_hi (xboxSet)
+  bool xboxSet = false;
   hg::UnitOrderCache order;           // star launch orders (boundary units last)
   std::shared_ptr<hg::JitKernel> jit;  // fused-apply family (generated, per program)
   std::vector<CUtensorMap> tmApply;   // per buffer, for the fused-apply boxes

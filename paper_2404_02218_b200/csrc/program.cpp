@@ -1088,4 +1088,34 @@ int hg_decompose_program(const hg_program *global, int ndim, const int64_t *grid
   return HG_OK;
 }
 
+int hg_decompose_program_deep(const hg_program *global, int ndim, const int64_t *grid,
+                              int depth, hg_program *local, hg_decomp *dc) {
+  if (depth < 1)
+    return setError(HG_EINVAL, "depth must be at least 1");
+  int st = hg_decompose_program(global, ndim, grid, local, dc);
+  if (st || depth == 1)
+    return st;
+  hg_program &out = *local;
+  const int r = out.rank;
+  const hg_bounds *stores = out.napplies > 0 ? out.mstore : out.store;
+  int64_t below[HG_MAX_FIELDS][3] = {}, above[HG_MAX_FIELDS][3] = {};
+  for (int f = 0; f < out.nfields; ++f)
+    for (int d = 0; d < r; ++d) {
+      const int64_t h = stores[0].lb[d] - out.fields[f].lb[d];
+      const int64_t H = grid[d] > 1 ? h * depth : h;
+      if (H > dc->core[d])
+        return setError(HG_EINVAL, "deep halo width " + std::to_string(H) +
+                                       " exceeds the per-rank core extent");
+      below[f][d] = above[f][d] = H;
+      out.fields[f].lb[d] = stores[0].lb[d] - H;
+      out.fields[f].ub[d] = stores[0].ub[d] + H;
+    }
+  for (int s = 0; s < dc->nswaps; ++s) {
+    const int f = dc->swaps[s].field;
+    dc->swaps[s].nexchanges = hg_exchanges(r, dc->core, below[f], above[f], nullptr, nullptr,
+                                           dc->swaps[s].ex, 2 * HG_MAX_RANK);
+  }
+  return HG_OK;
+}
+
 } // extern "C"

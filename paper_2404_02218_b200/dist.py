@@ -54,7 +54,7 @@ def origin_of(rank: int, grid: Sequence[int], core: Sequence[int]) -> List[int]:
 
 
 def make_dmp(plan, decomp, rank: int, grid: Sequence[int], world: int, transport: str = "p2p",
-             timeout_s: float = 0.0, group=None):
+             timeout_s: float = 0.0, depth: int = 1, group=None):
     """This rank's hg_dmp on the chosen transport, connected: P2P ranks exchange CUDA IPC
     blobs with their face neighbours; NCCL ranks share one ncclUniqueId (rank 0's)."""
     import torch.distributed as dist
@@ -64,7 +64,7 @@ def make_dmp(plan, decomp, rank: int, grid: Sequence[int], world: int, transport
         box = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0, group=group)
         return Dmp(plan, decomp, rank, transport="nccl", nccl_id=box[0], nranks=world,
-                   timeout_s=timeout_s)
-    dmp = Dmp(plan, decomp, rank, timeout_s=timeout_s)
+                   timeout_s=timeout_s, depth=depth)
+    dmp = Dmp(plan, decomp, rank, timeout_s=timeout_s, depth=depth)
     connect(dmp, rank, grid, world, group=group)
     return dmp

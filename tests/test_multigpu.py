@@ -230,3 +230,55 @@ def test_stuck_peer_reports_instead_of_hanging():
     r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "STUCK-PEER REPORTED" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,rank,order,extents,grid,T,calls,depth,transport", [
+    # deep halos (communication-avoiding): depth*h-wide halos exchanged
+    # every `depth` steps, the ring recomputed redundantly; odd call lengths end a round early
+    ("heat", 3, 4, "256x96x128", "2x1x1", 7, "3,4", 2, "p2p"),
+    ("heat", 3, 4, "256x96x256", "1x1x2", 6, "2,4", 2, "p2p"),     # packed x, extended region
+    ("wave", 3, 8, "400x48x96", "2x1x1", 7, "5,2", 2, "p2p"),
+    ("heat", 3, 2, "300x64x64", "2x1x1", 8, "8", 3, "p2p"),
+    ("heat", 2, 2, "512x256", "2x1", 9, "4,5", 3, "p2p"),
+    ("heat", 3, 4, "200x800x800", "2x1x1", 5, None, 2, "p2p"),     # wide tile, 1024-like planes
+    ("heat", 3, 4, "256x96x128", "2x1x1", 7, "3,4", 2, "nccl"),
+    ("wave", 3, 8, "200x96x192", "1x1x2", 5, None, 2, "nccl"),
+    ("heat", 3, 4, "192x128x256", "2x2x1", 6, "1,5", 2, "p2p"),
+    ("heat", 3, 4, "192x128x256", "1x2x2", 6, None, 2, "p2p"),
+])
+def test_ipc_dmp_deep_halo(kind, rank, order, extents, grid, T, calls, depth, transport):
+    n = _ngpus()
+    nproc = int(np.prod([int(x) for x in grid.split("x")]))
+    if n < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node",
+           str(nproc), os.path.join(REPO, "tools", "dmp_check.py"), "--kind", kind, "--rank",
+           str(rank), "--order", str(order), "--extents", extents, "--grid", grid, "--T",
+           str(T), "--depth", str(depth), "--transport", transport]
+    if calls:
+        cmd += ["--calls", calls]
+    r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec,grid,T,depth", [
+    (("heat", 3, 48, 4), [2, 1, 1], 7, 2), (("wave", 3, 48, 8), [1, 1, 2], 5, 2),
+    (("heat", 3, 64, 2), [2, 2, 1], 7, 3),
+])
+def test_simulate_deep_halo(port, spec, grid, T, depth):
+    # simulate with deep halos (one rank per GPU): gathered cores == the serial run
+    import paper_2404_02218_b200 as hg
+    n = _ngpus()
+    nr = int(np.prod(grid))
+    if n < nr:
+        pytest.skip(f"needs {nr} GPUs")
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    init = hg.initial_fields(prog)
+    out = hg.simulate(prog, grid, init, T, devices=list(range(nr)), depth=depth)
+    arrays = [b.data.copy() for b in init]
+    perm = port.run(prog, arrays, T)
+    for b, p in zip(out, perm):
+        assert np.array_equal(b.data.view(np.uint32), arrays[p].view(np.uint32))
