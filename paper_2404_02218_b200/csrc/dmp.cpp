@@ -319,6 +319,27 @@ int checkSticky(hg_dmp &d) {
   return c ? trapFrom(d, c) : HG_OK;
 }
 
+// Deep halos: the region of step ph of a round of kl steps -- the core extended by
+// (kl-1-ph)*unit toward every neighbour -- and per face the band of units whose loads reach
+// received cells (extension + radius).  Below the core in x (the contiguous dim) the
+// extension rounds up to 16 bytes so output rows stay 16-byte aligned: the extra columns are
+// computed from cells nobody exchanged and are never read (the next steps of the round read
+// less, and the round's data exchange rewrites the whole halo).
+void deepRegion(const hg_dmp &d, int ph, int kl, int64_t ext[][2], int *band) {
+  const hg_plan &p = *d.plan;
+  const int r = p.prog.rank;
+  const int64_t vec = 16 / p.lay[0].es;
+  for (int di = 0; di < 2 * r; ++di) {
+    if (d.nbr[di] < 0)
+      continue;
+    int64_t e = d.depth > 1 ? (kl - 1 - ph) * d.unit[di / 2] : 0;
+    if (e > 0 && di == 2 * (r - 1))
+      e = (e + vec - 1) / vec * vec;
+    ext[di / 2][di & 1] = e;
+    band[di] = static_cast<int>(e) + (starPlan(p) ? p.an.star.radius : 1);
+  }
+}
+
 // One time step of this rank on the flag (P2P) protocol: [ready handshake], stand-alone put
 // of what the previous step did not fuse, the stencil (halo-reading units wait in-kernel),
 // with the NEXT step's swap of the output fused into it unless this is the call's last step.
@@ -354,9 +375,8 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
   }
   const int ph = d.depth > 1 ? d.phase : 0, kl = d.depth > 1 ? d.klen : 1;
   int64_t ext[HG_MAX_RANK][2] = {{0, 0}, {0, 0}, {0, 0}};
-  for (int di = 0; di < 2 * r; ++di)
-    if (d.nbr[di] >= 0)
-      ext[di / 2][di & 1] = (kl - 1 - ph) * d.unit[di / 2];
+  int band[kDirs] = {0, 0, 0, 0, 0, 0};
+  deepRegion(d, ph, kl, ext, band);
   // 0. receiver-ready handshake after host uploads (hg_dmp_invalidate is collective): no
   //    neighbour may put into my buffers before my uploads into them are done
   const bool handshake = d.needReady;
@@ -409,6 +429,8 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
       p.regionExt[q][0] = ext[q][0];
       p.regionExt[q][1] = ext[q][1];
     }
+    for (int di = 0; di < kDirs; ++di)
+      p.band[di] = band[di];
     if (d.xpack && ph == 0 && packedRound) { // the cur buffer's x halo arrives packed
       const int xd = g.rank - 1;
       const int bCur =
@@ -469,7 +491,7 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     StarLaunch F{};
     for (int di = 0; di < 2 * r; ++di)
       if (d.nbr[di] >= 0) {
-        F.hs[di] = 1;
+        F.hs[di] = band[di]; // the units that read received cells in this step signal
         F.nodata |= 1 << di;
         F.peer_flag[di] = d.peerFlags[di];
       }
@@ -580,10 +602,17 @@ int ncclStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st) {
       d.klen = static_cast<int>(std::min<int64_t>(d.depth, steps - t));
   }
   const int ph = d.depth > 1 ? d.phase : 0, kl = d.depth > 1 ? d.klen : 1;
-  if (d.depth > 1)
-    for (int di = 0; di < 2 * r0; ++di)
-      if (d.nbr[di] >= 0)
-        p.regionExt[di / 2][di & 1] = (kl - 1 - ph) * d.unit[di / 2];
+  {
+    int64_t ext[HG_MAX_RANK][2] = {{0, 0}, {0, 0}, {0, 0}};
+    int band[kDirs] = {0, 0, 0, 0, 0, 0};
+    deepRegion(d, ph, kl, ext, band);
+    for (int q = 0; q < r0; ++q) {
+      p.regionExt[q][0] = ext[q][0];
+      p.regionExt[q][1] = ext[q][1];
+    }
+    for (int di = 0; di < kDirs; ++di)
+      p.band[di] = band[di];
+  }
   std::vector<Xjob> xs;
   if (ph == 0) // deep halos: one exchange per round
     if (int rc = collectJobs(d, xs))

@@ -254,7 +254,7 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
        "  const int n = min(P.chunk, P.nz - zb);\n"
        "  const int tid = threadIdx.x;\n"
        "  if (tid == 0) { for (int s = 0; s < NS; ++s) { mb_init(&full[s], 1); "
-       "mb_init(&empty[s], NCONS / 32); }\n"
+       "mb_init(&empty[s], NCONS); }\n"
        "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\"); }\n"
        "  __syncthreads();\n"
        "  if (n <= 0) return;\n";
@@ -275,7 +275,7 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
        "    return;\n"
        "  }\n";
   // consumers
-  s << "  const int tx = tid % TXT, ty = tid / TXT, lane = tid & 31, x0 = tx * 4;\n"
+  s << "  const int tx = tid % TXT, ty = tid / TXT, x0 = tx * 4;\n"
        "  const int rowOwn = (ty + RY) * CW + 4 + x0;\n"
     << "  const bool yok = " << (r == 3 ? "yb + ty < P.ny" : "true") << ";\n"
     << "  const int xrem = P.nx - (xb + x0);\n"
@@ -284,13 +284,14 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
     << "P.col0 + P.xs + xb + x0;\n"
        "  for (int i = 0; i < 2 * RZ; ++i) mb_wait(&full[i % NS], (u32)((i / NS) & 1));\n"
        "  int sOld = 0;          // stage of plane m (oldest in the window)\n"
+       "  long long ebase = obase; // output element of plane m\n"
        "  int sNew = (2 * RZ) % NS, phNew = ((2 * RZ) / NS) & 1;\n"
        "  for (int m = 0; m < n; ++m) {\n"
        "    mb_wait(&full[sNew], (u32)phNew);\n"
        "    if (++sNew == NS) { sNew = 0; phNew ^= 1; }\n";
   for (int dz = -rz; dz <= rz; ++dz)
-    s << "    const T *pl" << (dz + rz) << " = stages + (size_t)((sOld + " << (dz + rz)
-      << ") % NS) * O * SS;\n";
+    s << "    const T *pl" << (dz + rz) << " = stages + (size_t)(sOld + " << (dz + rz)
+      << " >= NS ? sOld + " << (dz + rz) << " - NS : sOld + " << (dz + rz) << ") * O * SS;\n";
   for (auto &[key, mask] : win) {
     auto [o, dz, dy] = key;
     std::string nm = "w" + std::to_string(o) + "_" + std::to_string(dz + rz) + "_" +
@@ -341,7 +342,7 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
     s << "    }\n";
   }
   s << "    if (yok) {\n"
-       "      const long long e = obase + (long long)m * P.plane;\n";
+       "      const long long e = ebase;\n";
   for (int k = 0; k < p.nresults; ++k)
     s << "      if (xrem >= 4) st4(P.out[" << k << "] + e, res" << k << "); else "
       << "for (int j = 0; j < 4; ++j) if (j < xrem) P.out[" << k << "][e + j] = res" << k
@@ -351,10 +352,11 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   // schedules LDS next to their first use, which may follow the arrive, and the SYNCS arrive
   // does not wait for in-flight LDS: the producer's next TMA then lands in the stage before
   // the load has read it (f64 windows, two LDS.128 each: flux3d per-apply tier, about 1 run
-  // in 10).  The arrive therefore follows the output stores, whose operands depend on every
-  // value the results use; a warp that stores nothing uses none of them.
-  s << "    __syncwarp();\n"
-       "    if (lane == 0) mb_arrive(&empty[sOld]);\n"
+  // in 10).  Every consumer thread therefore arrives after its own output stores, whose
+  // operands depend on every value its results use (the barrier counts all NCONS threads); a
+  // thread that stores nothing uses none of them.
+  s << "    ebase += P.plane;\n"
+       "    mb_arrive(&empty[sOld]);\n"
        "    if (++sOld == NS) sOld = 0;\n";
   s << "  }\n"
        "}\n";

@@ -144,6 +144,7 @@ template <typename T> struct StarParams {
   const unsigned long long *flags;
   unsigned long long epoch;
   int wmask;     // bit 2*dim + (sign > 0): a neighbour sends into that face
+  int band[6];   // units within band[d] of face d wait (their loads reach received cells)
   unsigned long long *err;        // bounded waits (waitFlag)
   unsigned long long timeout_ns;
   // packed x faces: slab [y][z][xw] of the cur buffer's lo/hi x halo, unpacked by the
@@ -191,11 +192,18 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int MINB =
       GEO == 1 ? 2 : GEO == 2 ? HG_MINB_G2
                    : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
+  // f32 3D radius <= 2: the ring is 2Q (heat SDO4) / 3Q (SDO2) slots deep, so the plane loop
+  // unrolled over one ring turn has compile-time slot indices (StarCfg::CT)
   static constexpr int DEPTH =
-      RANK == 3 ? (R <= 2 ? HG_DEPTH3 : (sizeof(T) == 8 ? 5 : HG_DEPTH3W)) : HG_DEPTH2;
+      RANK == 3 ? (R <= 2 ? (sizeof(T) == 4 && HG_ZP == 1 ? 7 : HG_DEPTH3)
+                          : (sizeof(T) == 8 ? 5 : HG_DEPTH3W))
+                : HG_DEPTH2;
   static constexpr int ZP = HG_ZP;                  // planes per ring slot
   static constexpr int NS = (R + 1 + DEPTH + ZP - 1) / ZP; // ring slots
   static constexpr int Q = 2 * R + 1;
+  // compile-time ring slots: the loop unrolls over NS planes (a multiple of the queue period)
+  static constexpr bool CT = ZP == 1 && NS % Q == 0;
+  static constexpr int UNROLL = CT ? NS : Q;
   static constexpr int STAGE = ROWS * CW;   // elements of one plane
   // one slot: ZP planes back to back (the TMA box layout), 128-byte aligned
   static constexpr int SSTRIDE = (ZP * STAGE + int(128 / sizeof(T)) - 1) / int(128 / sizeof(T)) * int(128 / sizeof(T));
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbarInit(&full[s], 1);
-      mbarInit(&empty[s], C::NWARPS_C);
+      mbarInit(&empty[s], C::NCONS); // every consumer thread arrives (no lane-0 branch)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -242,51 +250,80 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   if (n <= 0)
     return;
 
+  // dmp: the faces whose received cells this unit's loads reach (wait for the neighbour's
+  // round before loading them)
+  int need = 0;
+  if (P.flags) {
+    constexpr int XD = RANK - 1;
+    if (zb < P.band[0]) need |= 1;
+    if (zb + n > P.nz - P.band[1]) need |= 2;
+    if (RANK == 3 && yb < P.band[2]) need |= 4;
+    if (RANK == 3 && min(yb + C::TY, P.ny) > P.ny - P.band[3]) need |= 8;
+    if (xb < P.band[2 * XD]) need |= 1 << (2 * XD);
+    if (min(xb + C::TX, P.nx) > P.nx - P.band[2 * XD + 1]) need |= 2 << (2 * XD);
+    need &= P.wmask;
+  }
+  // packed x faces: the slab rows this unit's boxes read (its rows and y rim, its planes and
+  // z rim, clipped to the receive box) are unpacked into the halo columns by the whole CTA
+  // (many loads in flight), after the wait and before any TMA load
+  const int xunpack = (need >> (2 * (RANK - 1))) & ((P.xin[0] ? 1 : 0) | (P.xin[1] ? 2 : 0));
+  if (xunpack) {
+    if (tid == 0)
+      for (int di = 0; di < 6; ++di)
+        if (need & (1 << di))
+          waitFlag(P.flags + di, P.epoch, P.err, P.timeout_ns,
+                   (P.epoch << 8) | (unsigned long long)(di << 1) | 1ull);
+    __syncthreads();
+#pragma unroll 1
+    for (int sd = 0; sd < 2; ++sd) {
+      if (!(xunpack & (1 << sd)))
+        continue;
+      const T *slab = P.xin[sd];
+      const int W = P.xw[sd];
+      const int y0 = RANK == 3 ? max(P.xoy, yb - RY) : 0;
+      const int y1 = RANK == 3 ? min(P.xoy + P.xby, yb + C::TY + RY) : 1;
+      const int z0 = max(P.xoz, zb - R), z1 = min(P.xoz + P.xbz, zb + n + R);
+      const int per = (z1 - z0) * W;
+      const int total = (y1 - y0) * per;
+      const T *src0 = slab + (int64_t(y0 - P.xoy) * P.xbz + (z0 - P.xoz)) * W;
+      const int64_t rowStride = int64_t(P.xbz) * W;
+      T *dst0 = P.cur + int64_t(P.zs + z0) * P.plane +
+                (RANK == 3 ? int64_t(P.ys + y0) * P.pitch : 0) + P.col0 + P.xs + P.xox[sd];
+      constexpr int B = 4; // independent loads in flight per thread
+      for (int k0 = tid; k0 < total; k0 += B * C::NTHREADS) {
+        T v[B];
+        int64_t o[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int k = k0 + j * C::NTHREADS;
+          if (k < total) {
+            const int row = k / per, kk = k - row * per, dz = kk / W;
+            v[j] = src0[row * rowStride + kk];
+            o[j] = (RANK == 3 ? int64_t(row) * P.pitch : 0) + int64_t(dz) * P.plane +
+                   (kk - dz * W);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j)
+          if (k0 + j * C::NTHREADS < total)
+            dst0[o[j]] = v[j];
+      }
+    }
+    // the halo bytes arrived through the generic proxy; TMA reads via the async proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+  }
+
   if (tid >= C::NCONS) {
     // ---------------- producer warp ----------------
     const int plane_lane = tid - C::NCONS;
-    if (P.flags) {
-      constexpr int XD = RANK - 1;
-      int need = 0;
-      if (zb == 0) need |= 1;
-      if (zb + n >= P.nz) need |= 2;
-      if (RANK == 3 && yb == 0) need |= 4;
-      if (RANK == 3 && yb + C::TY >= P.ny) need |= 8;
-      if (xb == 0) need |= 1 << (2 * XD);
-      if (xb + C::TX >= P.nx) need |= 2 << (2 * XD);
-      need &= P.wmask;
-      if (plane_lane == 0)
-        for (int di = 0; di < 6; ++di)
-          if (need & (1 << di))
-            waitFlag(P.flags + di, P.epoch, P.err, P.timeout_ns,
-                     (P.epoch << 8) | (unsigned long long)(di << 1) | 1ull);
-      __syncwarp();
-      // packed x faces: the whole warp unpacks the slab rows this CTA's boxes read (its rows
-      // and y rim, its planes and z rim, clipped to the core) into the halo columns
-#pragma unroll 1
-      for (int sd = 0; sd < 2; ++sd) {
-        if (!(need & (1 << (2 * XD + sd))) || !P.xin[sd])
-          continue;
-        const T *slab = P.xin[sd];
-        const int W = P.xw[sd];
-        const int y0 = RANK == 3 ? max(P.xoy, yb - RY) : 0;
-        const int y1 = RANK == 3 ? min(P.xoy + P.xby, yb + C::TY + RY) : 1;
-        const int z0 = max(P.xoz, zb - R), z1 = min(P.xoz + P.xbz, zb + n + R);
-        const int per = (z1 - z0) * W;
-        const int64_t xoff = P.xox[sd];
-        for (int y = y0; y < y1; ++y) {
-          const T *src = slab + (int64_t(y - P.xoy) * P.xbz + (z0 - P.xoz)) * W;
-          T *dst = P.cur + int64_t(P.zs + z0) * P.plane +
-                   (RANK == 3 ? int64_t(P.ys + y) * P.pitch : 0) + P.col0 + P.xs + xoff;
-          for (int k = plane_lane; k < per; k += 32) {
-            const int dz = k / W;
-            dst[int64_t(dz) * P.plane + (k - dz * W)] = src[k];
-          }
-        }
-      }
+    if (need && !xunpack && plane_lane == 0) {
+      for (int di = 0; di < 6; ++di)
+        if (need & (1 << di))
+          waitFlag(P.flags + di, P.epoch, P.err, P.timeout_ns,
+                   (P.epoch << 8) | (unsigned long long)(di << 1) | 1ull);
       // the halo bytes arrived through the generic proxy; TMA reads via the async proxy
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      __syncwarp();
     }
     if (plane_lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur))
@@ -336,11 +373,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   const int rowOwn = (ty + RY) * C::CW;   // own row in a stage
   T q[Q][PTS];
 
-  auto release = [&](int s) {
-    __syncwarp();
-    if (lane == 0)
-      mbarArrive(&empty[s]);
-  };
+  auto release = [&](int s) { mbarArrive(&empty[s]); };
 
   constexpr int ZP = C::ZP;
   // prologue: planes 0 .. 2R-1 (z = zb-R .. zb+R-1): centres into the queue
@@ -363,6 +396,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   T *outRow = P.out + (int64_t(P.zs + zb) * P.plane +
                        (RANK == 3 ? int64_t(P.ys + yb + ty) * P.pitch : 0) + P.col0 + P.xs +
                        xb + x0);
+  T *dstPlane = outRow; // advanced by one plane per output plane (no per-plane multiply)
   const int xrem = P.nx - (xb + x0);
   // fused-swap geometry: faces this thread's row feeds (y) and x faces of its 4 points
   int blockTouch = 0;
@@ -381,15 +415,23 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   }
 
   // slot/sub-plane/parity of the plane arriving, slot/sub-plane of the plane being computed
+  // (runtime counters; with C::CT they are compile-time functions of U and the turn parity)
   int sN = ((2 * R) / ZP) % NS, zN = (2 * R) % ZP, phN = ((2 * R) / ZP / NS) & 1;
   int sC = (R / ZP) % NS, zC = R % ZP;
+  int turn = 0; // parity of the ring turn (C::CT: the loop advances one turn per iteration)
 
-  // One output plane; U is the position inside the Q-periodic register queue, a compile-time
-  // constant so every queue index below is a register name.  Returns false past the chunk end.
+  // One output plane; U is the position inside the unrolled loop body (a multiple of the
+  // Q-periodic register queue), a compile-time constant so every queue index below is a
+  // register name.  Returns false past the chunk end.
   auto plane = [&](int m, auto uc) -> bool {
     constexpr int U = decltype(uc)::value;
     if (m >= n)
       return false;
+    if constexpr (C::CT) {
+      sN = (U + 2 * R) % NS;
+      phN = turn ^ (((U + 2 * R) / NS) & 1);
+      sC = (U + R) % NS;
+    }
     // arrival of plane z+R: its centres enter the queue (one wait per slot)
     if (ZP == 1 || zN == 0)
       mbarWait(&full[sN], uint32_t(phN));
@@ -401,11 +443,13 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       for (int j = 0; j < 4; ++j)
         q[(U + 2 * R) % Q][4 * h + j] = c.v[j];
     }
-    if (++zN == ZP) {
-      zN = 0;
-      if (++sN == NS) {
-        sN = 0;
-        phN ^= 1;
+    if constexpr (!C::CT) {
+      if (++zN == ZP) {
+        zN = 0;
+        if (++sN == NS) {
+          sN = 0;
+          phN ^= 1;
+        }
       }
     }
     // x / y neighbours of plane z from its stage
@@ -430,10 +474,12 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
                     4 * h);
     // the slot is done once its last plane was the computed plane
     const int sDone = (ZP == 1 || zC == ZP - 1) ? sC : -1;
-    if (++zC == ZP) {
-      zC = 0;
-      if (++sC == NS)
-        sC = 0;
+    if constexpr (!C::CT) {
+      if (++zC == ZP) {
+        zC = 0;
+        if (++sC == NS)
+          sC = 0;
+      }
     }
 
     constexpr int cz = (U + R) % Q;
@@ -516,7 +562,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     }
     }
     if (yok) {
-      T *dst = outRow + int64_t(m) * P.plane;
+      T *dst = dstPlane;
       if (xrem >= PTS) {
 #pragma unroll
         for (int h = 0; h < NV; ++h)
@@ -528,12 +574,14 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
             dst[j] = o[j];
       }
     }
+    dstPlane += P.plane;
     // Release a stage only once the values read from it are consumed.  ptxas may schedule an
     // LDS after the arithmetic that precedes the arrive and complete it after the arrive (the
     // SYNCS arrive does not wait for in-flight LDS), so the producer's next TMA could land in
-    // the stage first: the arrive follows the output stores, whose operands depend on every
-    // value loaded from the stage.  A warp with no store (rows past the domain) uses none of
-    // them.  Planes 0..R-1 fed only the queue and go with the first output plane.
+    // the stage first: every consumer thread arrives (the barrier counts NCONS) after its own
+    // output stores, whose operands depend on every value it loaded from the stage.  A thread
+    // with no store (rows past the domain) uses none of them.  Planes 0..R-1 fed only the
+    // queue and go with the first output plane.
     if (sDone >= 0)
       release(sDone);
     if (m == 0) { // slots holding only planes 0..R-1 (never a computed plane)
@@ -544,8 +592,10 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     return true;
   };
 
-  for (int mb = 0; mb < n; mb += Q)
-    unrolled(plane, mb, std::make_integer_sequence<int, Q>{});
+  for (int mb = 0; mb < n; mb += C::UNROLL) {
+    unrolled(plane, mb, std::make_integer_sequence<int, C::UNROLL>{});
+    turn ^= 1;
+  }
 
   if (P.fuse && blockTouch) {
     // Fused swap of the next step: the send-box points this thread produced (re-read from its
@@ -663,15 +713,17 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
 // Launch order of the star units with every unit that touches a face in bmask (bit
 // 2*dim + hi; dims z, [y], x) after all the others, natural order within each group.  Built
 // once per geometry and cached by the plan; null (natural order) inside a stream capture.
-int unitOrder(UnitOrderCache &cache, int bmask, int rank, int tiles_x, int tiles_y, int nchunks,
-              int TX, int TY, int chunk, int nx, int ny, int nz, cudaStream_t st,
-              const int **perm, int *ninner) {
+int unitOrder(UnitOrderCache &cache, int bmask, const int *band, int rank, int tiles_x,
+              int tiles_y, int nchunks, int TX, int TY, int chunk, int nx, int ny, int nz,
+              cudaStream_t st, const int **perm, int *ninner) {
   *perm = nullptr;
   *ninner = 0;
-  const std::string key = std::to_string(bmask) + "/" + std::to_string(rank) + "/" +
+  std::string key = std::to_string(bmask) + "/" + std::to_string(rank) + "/" +
                           std::to_string(tiles_x) + "/" + std::to_string(tiles_y) + "/" +
                           std::to_string(nchunks) + "/" + std::to_string(TX) + "/" +
                           std::to_string(TY) + "/" + std::to_string(chunk);
+  for (int d = 0; d < 6; ++d)
+    key += "/" + std::to_string(band[d]);
   auto it = cache.tables.find(key);
   if (it != cache.tables.end()) {
     *perm = it->second;
@@ -691,12 +743,12 @@ int unitOrder(UnitOrderCache &cache, int bmask, int rank, int tiles_x, int tiles
     for (int ty = 0; ty < tiles_y; ++ty)
       for (int tx = 0; tx < tiles_x; ++tx) {
         int m = 0;
-        if (c == 0) m |= 1;
-        if ((c + 1) * chunk >= nz) m |= 2;
-        if (rank == 3 && ty == 0) m |= 4;
-        if (rank == 3 && (ty + 1) * TY >= ny) m |= 8;
-        if (tx == 0) m |= 1 << (2 * xd);
-        if ((tx + 1) * TX >= nx) m |= 2 << (2 * xd);
+        if (c * chunk < band[0]) m |= 1;
+        if (std::min((c + 1) * chunk, nz) > nz - band[1]) m |= 2;
+        if (rank == 3 && ty * TY < band[2]) m |= 4;
+        if (rank == 3 && std::min((ty + 1) * TY, ny) > ny - band[3]) m |= 8;
+        if (tx * TX < band[2 * xd]) m |= 1 << (2 * xd);
+        if (std::min((tx + 1) * TX, nx) > nx - band[2 * xd + 1]) m |= 2 << (2 * xd);
         const int u = (c * tiles_y + ty) * tiles_x + tx;
         (m & bmask ? outer : inner).push_back(u);
       }
@@ -787,6 +839,11 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   P.flags = L.wait_flags;
   P.epoch = L.wait_epoch;
   P.wmask = L.wait_mask;
+  for (int d = 0; d < 6; ++d) { // default: the units whose loads reach past the region
+    const int rd = d / 2 == 0 ? C::R : (RANK == 3 && d / 2 == 1 ? C::RY : C::R);
+    // units that send (fused swap) wait too: they store into halos the neighbour reads
+    P.band[d] = std::max(std::max(L.band[d] > 0 ? L.band[d] : rd, 1), L.fuse ? L.hs[d] : 0);
+  }
   P.err = L.err;
   P.timeout_ns = L.timeout_ns;
   P.cur = static_cast<T *>(L.cur);
@@ -881,8 +938,8 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   const unsigned blocks = unsigned(P.tiles_x) * P.tiles_y * P.nchunks;
   int ninner = int(blocks);
   if (bmask && L.order) {
-    int rc = unitOrder(*L.order, bmask, RANK, P.tiles_x, P.tiles_y, P.nchunks, C::TX, C::TY,
-                       P.chunk, P.nx, P.ny, P.nz, st, &P.perm, &ninner);
+    int rc = unitOrder(*L.order, bmask, P.band, RANK, P.tiles_x, P.tiles_y, P.nchunks, C::TX,
+                       C::TY, P.chunk, P.nx, P.ny, P.nz, st, &P.perm, &ninner);
     if (rc)
       return rc;
   }

@@ -50,6 +50,9 @@ struct StarLaunch {
   const unsigned long long *wait_flags = nullptr; // dmp: my flag words (null = no wait)
   unsigned long long wait_epoch = 0;
   int wait_mask = 0;
+  // per face: units whose region-relative extent comes within band[d] of face d read halo
+  // cells (or send) and wait; 0 = the stencil radius (the region is the core)
+  int band[6] = {0, 0, 0, 0, 0, 0};
   // bounded waits: after timeout_ns (0 = never) a waiter records (epoch << 8 | face << 1 | 1)
   // in *err and goes on (the host reports HG_ETRAP instead of the GPU hanging)
   unsigned long long *err = nullptr;

@@ -408,6 +408,10 @@ int planStep(hg_plan &p, cudaStream_t st) {
       L.xw[sd] = p.xw[sd];
     }
     L.split_event = p.splitEvent;
+    for (int d = 0; d < 6; ++d) {
+      L.band[d] = p.band[d];
+      p.band[d] = 0;
+    }
     L.split_mask = p.splitMask;
     p.waitFlags = nullptr;
     p.waitErr = nullptr;

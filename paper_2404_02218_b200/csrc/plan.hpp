@@ -46,6 +46,7 @@ struct hg_plan {
   // neighbours' points the next steps of the round need), and the packed x slabs' receive box
   // relative to that region
   int64_t regionExt[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  int band[6] = {0, 0, 0, 0, 0, 0};   // per face: units within band of it read received cells
   int xbox[6] = {0, 0, 0, 0, 0, 0}; // oz, oy, bz, by, ox_lo, ox_hi (xboxSet)
   bool xboxSet = false;
   hg::UnitOrderCache order;           // star launch orders (boundary units last)
