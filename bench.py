@@ -139,8 +139,8 @@ def cpu_baseline(workload="heat3d_weak"):
     (the interpreter is), on a bounded sample of the workload."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     from oracle import REF_PATH, Port, Ref
-    samples = {  # workload -> (kind, rank, extent, order, timesteps)
-        "heat3d_weak": ("heat", 3, 256, 4, 2), "heat3d_512": ("heat", 3, 256, 4, 2),
+    samples = {  # workload -> (kind, rank, extent, order, timesteps); slab = [8,1024,1024]
+        "heat3d_weak": ("slab", 3, (8, 1024, 1024), 4, 2), "heat3d_512": ("heat", 3, 256, 4, 2),
         "wave3d_1024": ("wave", 3, 160, 8, 2), "heat2d_1024": ("heat", 2, 1024, 2, 20),
         "pw_advection": ("pw", 3, (64, 128, 128), None, 1),
     }
@@ -151,6 +151,8 @@ def cpu_baseline(workload="heat3d_weak"):
         if kind == "pw":
             from paper_2404_02218_b200.programs.pw_advection import xir
             mod = ref.pipeline(ref.parse(xir(*ext)), "propagate-bounds")
+        elif kind == "slab":  # 1024^2 planes of config 5
+            mod = _slab_module(ref, ext[0])
         else:
             mod = ref.build(kind, rank, ext, order, True)
         bufs = ref.L.hr_initial_fields(mod)
@@ -160,6 +162,8 @@ def cpu_baseline(workload="heat3d_weak"):
         import paper_2404_02218_b200 as hg
         port = Port()
         prog = (hg.Program.pw_advection(*ext) if kind == "pw"
+                else hg.build_kernel(hg.KernelSpec("heat", 3, 8, 4, "f32")).with_extents(ext)
+                if kind == "slab"
                 else hg.build_kernel(hg.KernelSpec(kind, rank, ext, order, "f32")))
         arrays = port.initial_fields(prog)
         t0 = time.perf_counter()
@@ -167,7 +171,8 @@ def cpu_baseline(workload="heat3d_weak"):
         secs = time.perf_counter() - t0
         kindv = "port"
     return {"value": pts * timesteps / secs / 1e9, "unit": "GPts/s", "cores": 1, "kind": kindv,
-            "sample": f"{kind}{rank}d {ext if isinstance(ext, tuple) else f'{ext}^{rank}'} "
+            "sample": f"{'heat3d so4 slab' if kind == 'slab' else f'{kind}{rank}d'} "
+                      f"{list(ext) if isinstance(ext, tuple) else f'{ext}^{rank}'} "
                       f"x {timesteps} timesteps, runSerialStencil, 1 thread (host "
                       f"nproc={os.cpu_count()})",
             "seconds": secs}
@@ -242,21 +247,83 @@ def dead_on_arrival_bytes(prog, es):
     return total
 
 
-def _reference_worker(ext, warmup, steps, barrier, out):
-    """One host core: the reference's runSerialStencil on its own heat3d so4 ext^3 sample,
-    one timestep per bench step (oracle/_ref when built, else the C restatement)."""
+def workload_setup(args, world):
+    """The workload both arms report on: (global program or None, local program, decomposition
+    or None, grid, global core extents).  Host-only (the C-ABI's program functions)."""
+    import paper_2404_02218_b200 as hg
+    from paper_2404_02218_b200 import dist as hd
+    E = args.extent
+    if args.grid is not None:
+        grid = [int(x) for x in args.grid.split("x")]
+    else:
+        grid = hd.weak_grid(world) if args.mode == "weak" else hd.strong_grid(world)
+    assert int(grid[0] * grid[1] * grid[2]) == world
+    if args.mode == "weak":
+        gext = [E * grid[0], E * grid[1], E * grid[2]]  # E^3 per GPU
+    else:
+        gext = [args.strong_extent] * 3                 # fixed global domain
+    wl = WORKLOADS[args.workload]
+    if wl["kind"] == "heat3d":
+        glob = hg.build_kernel(hg.KernelSpec("heat", 3, E, 4, "f32")).with_extents(gext)
+        local, dc = glob.decompose(grid, depth=args.depth if world > 1 else 1)
+        return glob, local, dc, grid, gext
+    # single-GPU BASELINE configs; N > 1 runs independent replicas
+    local = wl["build"](hg)
+    return None, local, None, [1] * 3, core_extents(local)
+
+
+def workload_config(args, world, transport):
+    """The `config` object of the JSON line -- identical for both arms (--impl ours and
+    --impl reference), so the driver compares like with like."""
+    _, local, dc, grid, gext = workload_setup(args, world)
+    return {"workload": (f"heat3d_so4_{args.mode} (BASELINE config 5"
+                         f"{'; N=1 is the 1-GPU case' if args.mode == 'weak' else ''})")
+            if args.workload == "heat3d_weak" else WORKLOADS[args.workload]["desc"],
+            "core_per_gpu": list(dc.core[:3]) if dc is not None else None,
+            "global_core": gext if dc is not None else core_extents(local),
+            "grid": grid, "halo": halo_width(local), "halo_depth": args.depth,
+            "l2": ("8.4 MB of fields < 126 MB L2; by design they stay on chip "
+                   "(shared memory) for a whole run call, so no flush applies"
+                   if args.workload == "heat2d_1024" else
+                   f"inputs >> 126 MB L2 ({plan_bytes(local) / 1e9:.1f} GB of fields "
+                   f"per GPU), no flush needed"),
+            "transport": ("NCCL send/recv of packed boxes (C++, side stream, "
+                          "overlapped with the interior units)"
+                          if transport == "nccl" else
+                          "NVLink P2P stores fused into the stencil kernel (CUDA "
+                          "IPC) + system-scope flags; x faces as packed slabs")
+            if world > 1 else "none"}
+
+
+def _slab_module(ref, planes):
+    """The reference's own heat3d SDO4 step (exec::buildKernel, f32) over a [planes, 1024,
+    1024] slab of BASELINE config 5's domain: the printed 1024^3 module with dim 0's bounds
+    rewritten, re-parsed by the reference's parser (buildKernel only makes cubes,
+    kernels.cpp:155-158)."""
+    import re
+    txt = ref.print(ref.build("heat", 3, 1024, 4, True))
+    txt = re.sub(r"(<|\()\[(-?\d+),(\d+)\]x",
+                 lambda m: f"{m.group(1)}[{m.group(2)},{int(m.group(3)) - 1024 + planes}]x", txt)
+    return ref.parse(txt)
+
+
+def _reference_worker(planes, warmup, steps, barrier, out):
+    """One host core: the reference's runSerialStencil on its own [planes, 1024, 1024] slab of
+    the config-5 domain, one timestep per bench step (oracle/_ref when built, else the C
+    restatement)."""
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     from oracle import REF_PATH, Port, Ref
     if os.path.exists(REF_PATH):
         ref = Ref()
-        mod = ref.build("heat", 3, ext, 4, True)
+        mod = _slab_module(ref, planes)
         bufs = ref.L.hr_initial_fields(mod)
         step = lambda: ref.L.hr_time_serial(mod, bufs, 1)  # noqa: E731
         kind = "reference"
     else:
         import paper_2404_02218_b200 as hg
         port = Port()
-        prog = hg.build_kernel(hg.KernelSpec("heat", 3, ext, 4, "f32"))
+        prog = hg.build_kernel(hg.KernelSpec("heat", 3, 1024, 4, "f32")).with_extents(
+            [planes, 1024, 1024])
         arrays = port.initial_fields(prog)
 
         def step():
@@ -283,7 +350,7 @@ def run_reference(args):
     if rank != 0:
         return
     import multiprocessing as mp
-    ext = args.ref_extent
+    planes = args.ref_planes
     try:
         cores = len(os.sched_getaffinity(0))
     except Exception:
@@ -292,8 +359,8 @@ def run_reference(args):
         cores = min(cores, args.ref_procs)
     ctx = mp.get_context("spawn")
     barrier, out = ctx.Barrier(cores), ctx.Queue()
-    procs = [ctx.Process(target=_reference_worker, args=(ext, args.warmup, args.steps, barrier,
-                                                         out)) for _ in range(cores)]
+    procs = [ctx.Process(target=_reference_worker, args=(planes, args.warmup, args.steps,
+                                                         barrier, out)) for _ in range(cores)]
     for p in procs:
         p.start()
     res = [out.get() for _ in procs]
@@ -301,20 +368,20 @@ def run_reference(args):
         p.join()
     kind = res[0][0]
     total = max(t for _, t in res)
-    pts = ext ** 3
+    pts = planes * 1024 * 1024
     val = pts * args.steps * cores / total / 1e9
     out = {"metric": "GPts/s per step at 1/2/4/8 B200 (fraction of HBM roofline) vs host-CPU "
                      "reference", "value": val, "unit": "GPts/s",
            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference initValue)",
-           "config": {"workload": f"heat3d_so4 sample {ext}^3 per core per step (bounded sample "
-                                  f"of BASELINE config 5's 1024^3/GPU)", "timesteps_per_step": 1,
-                      "processes": cores},
+           "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+           "scaling": args.mode, "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (reference initValue hash, buffer.cpp:142-179)",
+           "config": workload_config(args, args.gpus, "p2p"),
            "cpu_baseline": {"value": val, "unit": "GPts/s", "cores": cores, "kind": kind,
-                            "sample": f"{cores} independent {ext}^3 heat3d so4 instances (one "
-                                      f"per host core), one runSerialStencil timestep each per "
-                                      f"bench step"},
+                            "sample": f"{cores} processes (one per host core; the interpreter "
+                                      f"is single-threaded), each advancing its own "
+                                      f"[{planes},1024,1024] slab of the config's 1024^2 planes "
+                                      f"by one runSerialStencil timestep per bench step"},
            "e2e": {"value": val, "unit": "GPts/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -341,24 +408,8 @@ def run_ours(args):
     sh = C.c_void_p(stream.cuda_stream)
 
     from paper_2404_02218_b200 import dist as hd
-    E = args.extent
-    if args.grid is not None:
-        grid = [int(x) for x in args.grid.split("x")]
-    else:
-        grid = hd.weak_grid(world) if args.mode == "weak" else hd.strong_grid(world)
-    assert int(grid[0] * grid[1] * grid[2]) == world
-    if args.mode == "weak":
-        gext = [E * grid[0], E * grid[1], E * grid[2]]  # E^3 per GPU
-    else:
-        gext = [args.strong_extent] * 3                 # fixed global domain
-    wl = WORKLOADS[args.workload]
-    if wl["kind"] == "heat3d":
-        glob = hg.build_kernel(hg.KernelSpec("heat", 3, E, 4, "f32")).with_extents(gext)
-        local, dc = glob.decompose(grid, depth=args.depth if world > 1 else 1)
-        origin = hd.origin_of(rank, grid, list(dc.core[:3]))
-    else:  # single-GPU BASELINE configs; N > 1 runs independent replicas
-        grid = [1] * 3
-        local, dc, origin = wl["build"](hg), None, None
+    glob, local, dc, grid, gext = workload_setup(args, world)
+    origin = hd.origin_of(rank, grid, list(dc.core[:3])) if dc is not None else None
     plan = hg.Plan(local, local_rank)
     plan.init_fields(origin=origin, stream=sh)
     dmp = None
@@ -502,24 +553,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": args.mode, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference initValue hash, buffer.cpp:142-179)",
-            "config": {"workload": (f"heat3d_so4_{args.mode} (BASELINE config 5"
-                                    f"{'; N=1 is the 1-GPU case' if args.mode == 'weak' else ''})")
-                       if args.workload == "heat3d_weak" else WORKLOADS[args.workload]["desc"],
-                       "kernel": plan.kernel_name,
-                       "core_per_gpu": list(dc.core[:3]) if dc is not None else None,
-                       "global_core": gext if dc is not None else core_extents(local),
-                       "grid": grid, "halo": halo_width(local), "halo_depth": args.depth,
-                       "l2": ("8.4 MB of fields < 126 MB L2; by design they stay on chip "
-                              "(shared memory) for a whole run call, so no flush applies"
-                              if args.workload == "heat2d_1024" else
-                              f"inputs >> 126 MB L2 ({plan_bytes(local) / 1e9:.1f} GB of fields "
-                              f"per GPU), no flush needed"),
-                       "transport": ("NCCL send/recv of packed boxes (C++, side stream, "
-                                     "overlapped with the interior units)"
-                                     if transport == "nccl" else
-                                     "NVLink P2P stores fused into the stencil kernel (CUDA "
-                                     "IPC) + system-scope flags; x faces as packed slabs")
-                       if world > 1 else "none"},
+            "config": workload_config(args, world, transport),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": plan.kernel_name, "kernel_ms": k_ms,
@@ -561,7 +595,8 @@ def main():
     ap.add_argument("--e2e-calls", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-extent", type=int, default=128)
+    ap.add_argument("--ref-planes", type=int, default=4,
+                    help="--impl reference: z planes of the [planes,1024,1024] slab per process")
     ap.add_argument("--ref-procs", type=int, default=0,
                     help="--impl reference: processes (default: every core this process may use)")
     args = ap.parse_args()
