@@ -1318,7 +1318,7 @@ template <typename T> __global__ void putKernel(const __grid_constant__ PutParam
     constexpr int VE = 16 / sizeof(T);
     const int64_t lastS = L.rank == 3 ? J.src_at[2] : (L.rank == 2 ? J.src_at[1] : J.src_at[0]);
     const int64_t lastD = L.rank == 3 ? J.dst_at[2] : (L.rank == 2 ? J.dst_at[1] : J.dst_at[0]);
-    const bool vec = L.rank >= 2 && w % VE == 0 && (L.col0 + lastS) % VE == 0 &&
+    const bool vec = L.rank >= 2 && w % VE == 0 && w >= 16 * VE && (L.col0 + lastS) % VE == 0 &&
                      (L.col0 + lastD) % VE == 0 && L.pitch % VE == 0;
     if (vec) {
       for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
@@ -1333,29 +1333,25 @@ template <typename T> __global__ void putKernel(const __grid_constant__ PutParam
           d4[c] = s4[c];
       }
     } else {
-      for (int64_t r = blockIdx.x; r < rowsEff; r += gridDim.x) {
-        int64_t i0, i1;
+      // any width (x faces: a few elements per row): one element per thread over the whole
+      // box, so narrow rows still keep every thread busy
+      const int64_t total = rowsEff * w;
+      for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
+           k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = k % w, r = k / w;
+        int64_t se, de;
         if (L.rank == 3) {
-          i0 = r / J.size[1];
-          i1 = r % J.size[1];
+          const int64_t i0 = r / J.size[1], i1 = r % J.size[1];
+          se = boxElem(L, J.src_at, i0, i1, c);
+          de = boxElem(L, J.dst_at, i0, i1, c);
+        } else if (L.rank == 2) {
+          se = boxElem(L, J.src_at, r, c, 0);
+          de = boxElem(L, J.dst_at, r, c, 0);
         } else {
-          i0 = r;
-          i1 = 0;
+          se = boxElem(L, J.src_at, c, 0, 0);
+          de = boxElem(L, J.dst_at, c, 0, 0);
         }
-        for (int64_t c = threadIdx.x; c < w; c += blockDim.x) {
-          int64_t se, de;
-          if (L.rank == 3) {
-            se = boxElem(L, J.src_at, i0, i1, c);
-            de = boxElem(L, J.dst_at, i0, i1, c);
-          } else if (L.rank == 2) {
-            se = boxElem(L, J.src_at, i0, c, 0);
-            de = boxElem(L, J.dst_at, i0, c, 0);
-          } else {
-            se = boxElem(L, J.src_at, c, 0, 0);
-            de = boxElem(L, J.dst_at, c, 0, 0);
-          }
-          dst[de] = src[se];
-        }
+        dst[de] = src[se];
       }
     }
   }
@@ -1685,9 +1681,10 @@ int launchPut(const PutJob *jobs, int njobs, const PutSignal *sig, int nsig,
     const DevLayout &L = jobs[j].lay;
     const int64_t rows = L.rank == 3 ? jobs[j].size[0] * jobs[j].size[1]
                                      : (L.rank == 2 ? jobs[j].size[0] : 1);
-    // packed jobs run one element per thread: rows of 256 elements
-    maxRows = std::max(maxRows, jobs[j].packed ? (rows * jobs[j].size[L.rank - 1] + 255) / 256
-                                               : rows);
+    // packed jobs and narrow (non-16-byte) rows run one element per thread
+    const int64_t w = jobs[j].size[L.rank - 1];
+    const bool flat = jobs[j].packed || w * L.es % 16 != 0 || w * L.es < 256;
+    maxRows = std::max(maxRows, flat ? (rows * w + 255) / 256 : rows);
     es = L.es;
   }
   dim3 grid(unsigned(std::min<int64_t>(maxRows, 1184)), unsigned(std::max(njobs, 1)));
