@@ -192,10 +192,12 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int MINB =
       GEO == 1 ? 2 : GEO == 2 ? HG_MINB_G2
                    : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
-  // f32 3D radius <= 2: the ring is 2Q (heat SDO4) / 3Q (SDO2) slots deep, so the plane loop
-  // unrolled over one ring turn has compile-time slot indices (StarCfg::CT)
+  // f32 3D radius <= 2 on the 64x16 tile: the ring is 2Q (heat SDO4) / 3Q (SDO2) slots deep,
+  // so the plane loop unrolled over one ring turn has compile-time slot indices (StarCfg::CT;
+  // heat 512^3 +4%).  The wide 128x12 tile keeps the 8-slot ring: at 10 slots its DRAM reads
+  // grew 5% (ncu: 4.76 -> 5.01 GB per 1024^3 step) and it ran 4% slower (A/B on one box).
   static constexpr int DEPTH =
-      RANK == 3 ? (R <= 2 ? (sizeof(T) == 4 && HG_ZP == 1 ? 7 : HG_DEPTH3)
+      RANK == 3 ? (R <= 2 ? (sizeof(T) == 4 && HG_ZP == 1 && GEO == 0 ? 7 : HG_DEPTH3)
                           : (sizeof(T) == 8 ? 5 : HG_DEPTH3W))
                 : HG_DEPTH2;
   static constexpr int ZP = HG_ZP;                  // planes per ring slot

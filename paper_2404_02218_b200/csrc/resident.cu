@@ -97,15 +97,26 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
   const int ngx = (P.nx + 3) / 4;
   const int gy0 = tid / ngx, gx0 = tid % ngx, dgy = NTH / ngx, dgx = NTH % ngx;
   const int cx = P.PL + P.s0c; // shared column of store column 0 (16-byte aligned)
+  // shared-memory offsets stay 32-bit (a tile is < 227 KB): no 64-bit address math per item
+  const int SP = P.SP;
+  const int rowBase = (P.s0r - lo) * SP + cx; // offset of (store row 0, store column 0)
   const bool vec = (P.nx & 3) == 0; // exchange rows move as 16-byte vectors
   int cur = 0;
   int done = 0, blk = 0;
   while (done < P.steps) {
     const int kk = min(P.K, P.steps - done);
+    // f32: the last sub-step before an exchange stores its boundary rows' values straight
+    // into my exchange slot as tagged words while it computes them (no separate copy pass)
+    using W64 = unsigned long long;
+    const bool xchNext = sizeof(T) == 4 && done + kk < P.steps;
+    W64 *const mineX = reinterpret_cast<W64 *>(P.xbuf) +
+                       (size_t(blk & 1) * G + c) * 2 * (size_t(E) * P.nx);
+    const W64 tagX = W64(P.tag0 + unsigned(blk) + 1u) << 32;
     for (int s = 0; s < kk; ++s) {
+      const bool xch = xchNext && s == kk - 1;
       const int ylo = max(0, r0 - (kk - 1 - s) * R), yhi = min(P.ny, r1 + (kk - 1 - s) * R);
-      const T *in = tile(cur);
-      T *out = tile(cur ^ 1);
+      const T *in = cur ? tile1 : tile0;
+      T *out = cur ? tile0 : tile1;
       // work items: 4 points in each of two consecutive rows (y, y+1), row-pair-major from
       // (ylo, 0); the two rows share their column neighbours' loads (2R+6 LDS.128 for 8
       // points instead of 2(2R+3)).  This thread's walk needs no division.
@@ -114,18 +125,18 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
            gx += dgx, pr += dgy + (gx >= ngx ? 1 : 0), gx -= gx >= ngx ? ngx : 0) {
         const int y = ylo + 2 * pr, x0 = gx * 4;
         const bool two = y + 1 < yhi;
-        const int i = P.s0r + y - lo; // tile row of y
-        const T *row = in + size_t(i) * P.SP + cx + x0;
+        const int off = rowBase + y * SP + x0; // tile offset of (y, x0)
+        const T *row = in + off;
         V4<T> cen[2 * R + 2]; // centres of rows y-R .. y+1+R
 #pragma unroll
         for (int d = 0; d < 2 * R + 2; ++d)
           if (d != 2 * R + 1 || two)
-            cen[d] = ld4(row + (d - R) * P.SP);
+            cen[d] = ld4(row + (d - R) * SP);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           if (h == 1 && !two)
             break;
-          const V4<T> L = ld4(row + h * P.SP - 4), Rr = ld4(row + h * P.SP + 4);
+          const V4<T> L = ld4(row + h * SP - 4), Rr = ld4(row + h * SP + 4);
           const V4<T> &Cc = cen[R + h];
           V4<T> o;
 #pragma unroll
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
             }
             o.v[j] = add_(cc, mul_(acc, P.scale));
           }
-          T *dst = out + size_t(i + h) * P.SP + cx + x0;
+          T *dst = out + off + h * SP;
           if (x0 + 4 <= P.nx) {
             st4(dst, o);
           } else { // the ring columns right of the store box stay untouched
@@ -156,9 +167,31 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
               if (x0 + j < P.nx)
                 dst[j] = o.v[j];
           }
+          if constexpr (sizeof(T) == 4) {
+            if (xch) {
+              // slot rows: [0, E) = my first E rows, [E, 2E) = my last E rows (a row can be
+              // both in a band of fewer than 2E rows)
+              const int yy = y + h;
+              for (int side = 0; side < 2; ++side) {
+                const int r = side == 0 ? yy - r0 : E + yy - (r1 - E);
+                if (side == 0 ? yy - r0 >= E : yy < r1 - E)
+                  continue;
+                W64 *m = mineX + size_t(r) * P.nx + x0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  if (x0 + j < P.nx)
+                    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(m + j),
+                                 "l"(tagX | __float_as_uint(o.v[j]))
+                                 : "memory");
+              }
+            }
+          }
         }
       }
-      __syncthreads();
+      // (before an exchange the halo rows the poll below writes are not read by this
+      // sub-step, and its boundary values already went out: the poll needs no barrier first)
+      if (!xch)
+        __syncthreads();
       cur ^= 1;
     }
     done += kk;
@@ -172,52 +205,41 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
       // word itself is the flag (single-copy atomic): no fence, no flag round trip.  Slot
       // reuse two blocks later is safe: a CTA overwrites slot `par` only after it has read the
       // neighbour's NEXT block, which the neighbour computed from this one.
-      using W64 = unsigned long long;
       W64 *xw = reinterpret_cast<W64 *>(P.xbuf);
-      const W64 tg = W64(P.tag0 + unsigned(blk) + 1u) << 32;
-      W64 *mine = xw + (size_t(par) * G + c) * 2 * slot;
-      const T *t = tile(cur);
-      for (int r = 0; r < 2 * E; ++r) {
-        const int y = r < E ? r0 + r : r1 - 2 * E + r;
-        const T *src = t + size_t(P.s0r + y - lo) * P.SP + cx;
-        for (int x = tid; x < P.nx; x += NTH) {
-          const W64 w = tg | __float_as_uint(src[x]);
-          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(mine + size_t(r) * P.nx + x),
-                       "l"(w)
-                       : "memory");
-        }
-      }
-      T *tw = tile(cur);
-      // row r of the 2E halo rows: its source word and its destination in the tile
-      auto srcRow = [&](int r) {
-        const bool top = r < E;
-        return xw + (size_t(par) * G + (top ? c - 1 : c + 1)) * 2 * slot + (top ? slot : 0) +
-               size_t(top ? r : r - E) * P.nx;
-      };
-      auto dstRow = [&](int r) {
-        const int y = r < E ? r0 - E + r : r1 + r - E;
-        return tw + size_t(P.s0r + y - lo) * P.SP + cx;
-      };
-      auto live = [&](int r) { return r < E ? c > 0 : c + 1 < G; };
+      const W64 tg = tagX;
+      T *tw = cur ? tile1 : tile0;
+      const int nx = P.nx;
+      // the neighbours' rows: row r of my 2E halo rows (r < E: above, from the upper band's
+      // last E rows; else below, from the lower band's first E rows)
+      const W64 *above = xw + (size_t(par) * G + (c - 1)) * 2 * slot + slot;
+      const W64 *below = xw + (size_t(par) * G + (c + 1)) * 2 * slot;
+      const bool hasAbove = c > 0, hasBelow = c + 1 < G;
       auto ldw = [](const W64 *q) {
         W64 w;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(q) : "memory");
         return w;
       };
+      auto srcOf = [&](int r, int x) {
+        return r < E ? above + size_t(r) * nx + x : below + size_t(r - E) * nx + x;
+      };
+      auto dstOf = [&](int r) { // tile offset of halo row r at store column 0
+        return rowBase + (r < E ? r0 - E + r : r1 + r - E) * SP;
+      };
+      auto live = [&](int r) { return r < E ? hasAbove : hasBelow; };
       constexpr int MW = 4; // up to 4 halo rows (K=2, R=1) polled concurrently: one round trip
-      for (int x = tid; x < P.nx; x += NTH) {
+      for (int x = tid; x < nx; x += NTH) {
         if (2 * E <= MW) {
           W64 w[MW];
 #pragma unroll
           for (int r = 0; r < MW; ++r)
             if (r < 2 * E && live(r))
-              w[r] = ldw(srcRow(r) + x);
+              w[r] = ldw(srcOf(r, x));
 #pragma unroll
           for (int r = 0; r < MW; ++r)
             if (r < 2 * E && live(r)) {
               while ((w[r] & ~0xffffffffull) != tg)
-                w[r] = ldw(srcRow(r) + x);
-              dstRow(r)[x] = __uint_as_float(unsigned(w[r]));
+                w[r] = ldw(srcOf(r, x));
+              tw[dstOf(r) + x] = __uint_as_float(unsigned(w[r]));
             }
         } else {
           for (int r = 0; r < 2 * E; ++r) {
@@ -225,9 +247,9 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
               continue;
             W64 w;
             do {
-              w = ldw(srcRow(r) + x);
+              w = ldw(srcOf(r, x));
             } while ((w & ~0xffffffffull) != tg);
-            dstRow(r)[x] = __uint_as_float(unsigned(w));
+            tw[dstOf(r) + x] = __uint_as_float(unsigned(w));
           }
         }
       }

@@ -36,9 +36,26 @@ def test_workload_config_fields(workload, core, halo):
 
 def test_reference_arm_uses_the_given_cores():
     r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
-                        "--steps", "1", "--warmup", "1", "--ref-extent", "24", "--ref-procs",
+                        "--steps", "1", "--warmup", "1", "--ref-planes", "1", "--ref-procs",
                         "2"], capture_output=True, text=True, timeout=600, cwd=REPO)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["cpu_baseline"]["cores"] == 2
     assert line["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_reference_arm_reports_our_config():
+    # the driver compares the two arms' lines: same metric, unit, direction and config
+    import argparse
+    a = argparse.Namespace(extent=1024, grid=None, mode="weak", workload="heat3d_weak",
+                           depth=1, strong_extent=2048)
+    c1 = bench.workload_config(a, 1, "p2p")
+    assert c1["core_per_gpu"] == [1024, 1024, 1024] and c1["grid"] == [1, 1, 1]
+    assert c1["halo"] == 2 and "kernel" not in c1
+
+
+def test_reference_slab_module_is_config5_planes(ref):
+    # the reference arm's sample: the reference's own 1024^3 heat SDO4 module, dim 0 narrowed
+    mod = bench._slab_module(ref, 3)
+    txt = ref.print(mod)
+    assert "[-2,5]x[-2,1026]x[-2,1026]xf32" in txt and "([0,3]x[0,1024]x[0,1024])" in txt

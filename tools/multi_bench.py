@@ -20,7 +20,7 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record(); plan.run(T); e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
 l = plan.launch_count()
-print(plan.kernel_name, "%%.1f GPts/s" %% (n ** 3 * T / ms / 1e6), "(8 B/pt ideal -> %%.2f of HBM)" %% (n ** 3 * T / ms / 1e6 * 8 / 6538.9))
+print(plan.kernel_name, "%%.1f GPts/s" %% (n ** 3 * T / ms / 1e6), "(8 B/pt ideal -> %%.2f of HBM)" %% (n ** 3 * T / ms / 1e6 * 8 / 6451.8))
 '''
 
 if __name__ == "__main__":
