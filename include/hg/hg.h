@@ -275,6 +275,11 @@ int hg_plan_unpack(hg_plan *plan, int buffer, const int64_t *at, const int64_t *
 /* Tuning knobs of the star family: z-chunks per column tile (0 = auto) and whether the
  * z-boundary chunks run last (lets halo exchange overlap interior compute). */
 int hg_plan_set_tuning(hg_plan *plan, int chunks, int boundary_last);
+/* Debug builds of a run (HG_DEBUG_GUARDS=1 at plan creation): every device buffer of the plan
+ * sits between 64 KB canary bands; HG_ETRAP if any kernel wrote into one (the memcheck-style
+ * out-of-bounds-write check this pool allows: compute-sanitizer is closed here).  HG_OK
+ * without guards. */
+int hg_plan_check_guards(hg_plan *plan);
 /* Block until all work queued for the plan's device has finished. */
 int hg_plan_synchronize(hg_plan *plan);
 /* Kernel launches issued by this plan so far (for bench/gpu_launches accounting). */

@@ -13,6 +13,8 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
+import os
+
 from . import _capi as capi
 from ._capi import HgDecomp, HgError, HgExchange, HgLayout, HgOp, HgProgram, check, lib  # noqa: F401
 
@@ -359,6 +361,9 @@ def initial_fields(prog: Program) -> List[Buffer]:
 
 
 # ---- plans -------------------------------------------------------------------------------------
+_GUARDS = os.environ.get("HG_DEBUG_GUARDS", "") not in ("", "0")
+
+
 class Plan:
     """Device-resident fields + compiled step (hg_plan)."""
 
@@ -371,8 +376,16 @@ class Plan:
 
     def close(self):
         if self.h:
-            lib().hg_plan_destroy(self.h)
-            self.h = None
+            h, self.h = self.h, None
+            try:
+                if _GUARDS:  # debug runs: no kernel may have written outside its buffers
+                    check(lib().hg_plan_check_guards(h))
+            finally:
+                lib().hg_plan_destroy(h)
+
+    def check_guards(self):
+        """HG_DEBUG_GUARDS=1 plans: raise HgError(HG_ETRAP) on an out-of-bounds write."""
+        check(lib().hg_plan_check_guards(self.h))
 
     def __del__(self):
         try:

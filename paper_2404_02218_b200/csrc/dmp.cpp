@@ -49,6 +49,8 @@ struct Blob {
   int64_t rank;
   uint64_t layoutHash;
   int64_t slabElems;
+  int64_t bufOffset[HG_MAX_FIELDS]; // buffer pointer - allocation base (HG_DEBUG_GUARDS)
+  int64_t slabOffset;
   cudaIpcMemHandle_t flags;
   cudaIpcMemHandle_t slab;
   cudaIpcMemHandle_t buf[HG_MAX_FIELDS];
@@ -134,7 +136,9 @@ struct hg_dmp {
   int64_t coord[HG_MAX_RANK] = {0, 0, 0};
   int64_t nbr[kDirs];
   void *peer[kDirs][HG_MAX_FIELDS] = {};
+  void *peerBase[kDirs][HG_MAX_FIELDS] = {}; // what cudaIpcOpenMemHandle returned
   char *peerSlab[kDirs] = {};          // the neighbour's slab allocation
+  void *peerSlabBase[kDirs] = {};
   unsigned long long *peerFlags[kDirs] = {};
   bool opened[kDirs] = {};
   unsigned long long *flags = nullptr; // my flag words (kFlagBytes)
@@ -245,11 +249,15 @@ int collectJobs(hg_dmp &d, std::vector<Xjob> &out) {
   return HG_OK;
 }
 
-// P2P put jobs of this step (x faces into the neighbours' slabs when packed).
-int buildPutJobs(hg_dmp &d, std::vector<PutJob> &jobs, bool xpack) {
+// P2P put jobs of this step (x faces into the neighbours' slabs when packed); `sent`, when
+// given, receives the exchanges (the neighbours send me the mirror image of them).
+int buildPutJobs(hg_dmp &d, std::vector<PutJob> &jobs, bool xpack,
+                 std::vector<Xjob> *sent = nullptr) {
   std::vector<Xjob> xs;
   if (int rc = collectJobs(d, xs))
     return rc;
+  if (sent)
+    *sent = xs;
   hg_plan &p = *d.plan;
   const int r = p.prog.rank;
   for (const Xjob &x : xs) {
@@ -403,11 +411,11 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
       return rc;
     ++p.launches;
   }
-  // 1. stand-alone put of every dirty swapped buffer, straight into the neighbours' halos
-  //    (x faces too: only rounds a fused put produced arrive as packed slabs)
-  const bool packedRound = d.roundReady;
+  // 1. stand-alone put of every dirty swapped buffer (x faces packed into the neighbours'
+  //    slabs; the symmetric dirty state tells me which of my slabs the neighbours fill)
   std::vector<PutJob> jobs;
-  if (int rc = buildPutJobs(d, jobs, false))
+  std::vector<Xjob> sent;
+  if (int rc = buildPutJobs(d, jobs, d.xpack, d.xpack ? &sent : nullptr))
     return rc;
   mark();
   if (!d.roundReady || !jobs.empty()) {
@@ -418,6 +426,41 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     if (nsig || !jobs.empty())
       ++p.launches;
   }
+  // x slabs of buffers other than this step's cur (e.g. wave's prev on a call's first step):
+  // unpacked here, once the round is in; the stencil kernel unpacks cur's slab itself
+  {
+    const int bCurNow = star ? p.bind[static_cast<size_t>(g.operand_field[p.an.star.cur_operand])]
+                             : -1;
+    bool waited = false;
+    for (const Xjob &x : sent) {
+      if (x.dim != g.rank - 1 || (star && x.buffer == bCurNow))
+        continue;
+      if (!waited) {
+        if (int rc = launchWaitFlags(d.flags, widx, nw, d.epoch, err, d.timeoutNs, st))
+          return rc;
+        ++p.launches;
+        waited = true;
+      }
+      // my receive box on that face: the `at` of my exchange toward the sender
+      int64_t at[3];
+      for (int q = 0; q < 3; ++q)
+        at[q] = x.recv_at[q]; // same template both ways (mate's at == my at for my face)
+      const hg_swap &sw0 = d.dc.swaps[x.swap];
+      for (int k = 0; k < sw0.nexchanges; ++k) {
+        int dim2, sign2;
+        dirOf(sw0.ex[k], g.rank, &dim2, &sign2);
+        if (dirIndex(dim2, sign2) == x.dir)
+          for (int q = 0; q < g.rank; ++q)
+            at[q] = sw0.ex[k].at[q];
+      }
+      if (int rc = launchSlabUnpack(p.dptr[static_cast<size_t>(x.buffer)],
+                                    devLayout(p.lay[static_cast<size_t>(x.buffer)]), at, x.size,
+                                    d.slab + slabOffset(d, x.buffer, x.dir & 1), st))
+        return rc;
+      ++p.launches;
+    }
+  }
+  const bool packedRound = d.xpack;
   // 2. the stencil step; halo-reading CTAs wait for the round in-kernel
   if (star && nw) {
     p.waitFlags = d.flags;
@@ -730,17 +773,18 @@ void freeDmp(hg_dmp *d) {
     for (int di = 0; di < kDirs; ++di)
       if (d->opened[di]) {
         for (int b = 0; b < HG_MAX_FIELDS; ++b)
-          if (d->peer[di][b])
-            cudaIpcCloseMemHandle(d->peer[di][b]);
+          if (d->peerBase[di][b])
+            cudaIpcCloseMemHandle(d->peerBase[di][b]);
         if (d->peerFlags[di])
           cudaIpcCloseMemHandle(d->peerFlags[di]);
-        if (d->peerSlab[di])
-          cudaIpcCloseMemHandle(d->peerSlab[di]);
+        if (d->peerSlabBase[di])
+          cudaIpcCloseMemHandle(d->peerSlabBase[di]);
       }
   cudaFree(d->flags);
   cudaFree(d->counter);
   cudaFree(d->cnt6);
-  cudaFree(d->slab);
+  if (d->slab)
+    planFree(*d->plan, d->slab);
   if (d->errHost)
     cudaFreeHost(d->errHost);
   if (d->putDone)
@@ -864,8 +908,10 @@ int hg_dmp_create_ex(hg_plan *plan, const hg_decomp *dc, int64_t rank, const hg_
       return st;
     if (d->xpack) {
       const size_t bytes = slabOffset(*d, static_cast<int>(plan->dptr.size()), 0);
-      if (int st = cudaCheck(cudaMalloc(&d->slab, bytes), "cudaMalloc(x slabs)"))
+      void *sl = nullptr; // guarded like the plan's buffers under HG_DEBUG_GUARDS
+      if (int st = planAlloc(*plan, &sl, bytes, "cudaMalloc(x slabs)"))
         return st;
+      d->slab = static_cast<char *>(sl);
     }
     if (int st = cudaCheck(cudaMallocHost(&d->errHost, sizeof(unsigned long long)),
                            "cudaMallocHost(err)"))
@@ -947,13 +993,18 @@ int hg_dmp_ipc_export(hg_dmp *d, void *blob, size_t cap, size_t *len) {
     return st;
   if (int st = cudaCheck(cudaIpcGetMemHandle(&b.flags, d->flags), "cudaIpcGetMemHandle(flags)"))
     return st;
-  if (d->slab)
-    if (int st = cudaCheck(cudaIpcGetMemHandle(&b.slab, d->slab), "cudaIpcGetMemHandle(slab)"))
+  if (d->slab) {
+    b.slabOffset = d->slab - static_cast<char *>(planAllocBase(*d->plan, d->slab));
+    if (int st = cudaCheck(cudaIpcGetMemHandle(&b.slab, planAllocBase(*d->plan, d->slab)),
+                           "cudaIpcGetMemHandle(slab)"))
       return st;
-  for (uint32_t i = 0; i < b.nbuf; ++i)
-    if (int st = cudaCheck(cudaIpcGetMemHandle(&b.buf[i], d->plan->dptr[i]),
-                           "cudaIpcGetMemHandle"))
+  }
+  for (uint32_t i = 0; i < b.nbuf; ++i) {
+    void *base = planAllocBase(*d->plan, d->plan->dptr[i]);
+    b.bufOffset[i] = static_cast<char *>(d->plan->dptr[i]) - static_cast<char *>(base);
+    if (int st = cudaCheck(cudaIpcGetMemHandle(&b.buf[i], base), "cudaIpcGetMemHandle"))
       return st;
+  }
   std::memcpy(blob, &b, sizeof b);
   return HG_OK;
 }
@@ -985,14 +1036,16 @@ int hg_dmp_ipc_import(hg_dmp *d, int64_t peer, const void *blob, size_t len) {
       if (int st = cudaCheck(cudaIpcOpenMemHandle(&s, b.slab, cudaIpcMemLazyEnablePeerAccess),
                              "cudaIpcOpenMemHandle(slab)"))
         return st;
-      d->peerSlab[di] = static_cast<char *>(s);
+      d->peerSlabBase[di] = s;
+      d->peerSlab[di] = static_cast<char *>(s) + b.slabOffset;
     }
     for (uint32_t i = 0; i < b.nbuf; ++i) {
       void *p = nullptr;
       if (int st = cudaCheck(cudaIpcOpenMemHandle(&p, b.buf[i], cudaIpcMemLazyEnablePeerAccess),
                              "cudaIpcOpenMemHandle(buffer)"))
         return st;
-      d->peer[di][i] = p;
+      d->peerBase[di][i] = p;
+      d->peer[di][i] = static_cast<char *>(p) + b.bufOffset[i];
     }
     d->opened[di] = true;
   }

@@ -712,18 +712,64 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   }
 }
 
-// Launch order of the star units with every unit that touches a face in bmask (bit
-// 2*dim + hi; dims z, [y], x) after all the others, natural order within each group.  Built
-// once per geometry and cached by the plan; null (natural order) inside a stream capture.
+// Unit geometry for the launch order: does unit u (x tile fastest, then y tile, then z chunk)
+// touch a face in bmask (bit 2*dim + hi; dims z, [y], x), i.e. come within band[d] of it?
+struct UnitGeom {
+  int bmask, rank, tiles_x, tiles_y, nchunks, TX, TY, chunk, nx, ny, nz;
+  int band[6];
+};
+
+__host__ __device__ inline bool unitTouches(const UnitGeom &g, int u) {
+  const int tx = u % g.tiles_x, ty = (u / g.tiles_x) % g.tiles_y, c = u / (g.tiles_x * g.tiles_y);
+  const int xd = g.rank - 1;
+  int m = 0;
+  if (c * g.chunk < g.band[0]) m |= 1;
+  if (min((c + 1) * g.chunk, g.nz) > g.nz - g.band[1]) m |= 2;
+  if (g.rank == 3 && ty * g.TY < g.band[2]) m |= 4;
+  if (g.rank == 3 && min((ty + 1) * g.TY, g.ny) > g.ny - g.band[3]) m |= 8;
+  if (tx * g.TX < g.band[2 * xd]) m |= 1 << (2 * xd);
+  if (min((tx + 1) * g.TX, g.nx) > g.nx - g.band[2 * xd + 1]) m |= 2 << (2 * xd);
+  return (m & g.bmask) != 0;
+}
+
+// The launch-order table, built on the device by one CTA (a stable partition: interior units
+// in natural order, then the boundary units), so building it never blocks the host -- a
+// synchronous copy here could wait behind a kernel spinning on a peer's flag.
+__global__ void __launch_bounds__(1024) unitOrderKernel(int *out, int total, int ninner,
+                                                        const UnitGeom g) {
+  __shared__ int scan[1024];
+  const int t = threadIdx.x, per = (total + 1023) / 1024;
+  const int a = min(total, t * per), b = min(total, a + per);
+  int cnt = 0;
+  for (int u = a; u < b; ++u)
+    cnt += unitTouches(g, u) ? 0 : 1;
+  scan[t] = cnt;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) { // inclusive Hillis-Steele scan
+    const int v = t >= off ? scan[t - off] : 0;
+    __syncthreads();
+    scan[t] += v;
+    __syncthreads();
+  }
+  int in = scan[t] - cnt;        // interior units before my range
+  int bd = ninner + (a - in);    // boundary slots before my range
+  for (int u = a; u < b; ++u)
+    out[unitTouches(g, u) ? bd++ : in++] = u;
+}
+
+// Launch order of the star units with every unit that touches a face in bmask (within
+// band[d] of face d; dims z, [y], x) after all the others, natural order within each group.
+// Built once per geometry and cached by the plan; null (natural order) inside a stream
+// capture.  Nothing here synchronizes the host with the device.
 int unitOrder(UnitOrderCache &cache, int bmask, const int *band, int rank, int tiles_x,
               int tiles_y, int nchunks, int TX, int TY, int chunk, int nx, int ny, int nz,
               cudaStream_t st, const int **perm, int *ninner) {
   *perm = nullptr;
   *ninner = 0;
   std::string key = std::to_string(bmask) + "/" + std::to_string(rank) + "/" +
-                          std::to_string(tiles_x) + "/" + std::to_string(tiles_y) + "/" +
-                          std::to_string(nchunks) + "/" + std::to_string(TX) + "/" +
-                          std::to_string(TY) + "/" + std::to_string(chunk);
+                    std::to_string(tiles_x) + "/" + std::to_string(tiles_y) + "/" +
+                    std::to_string(nchunks) + "/" + std::to_string(TX) + "/" +
+                    std::to_string(TY) + "/" + std::to_string(chunk);
   for (int d = 0; d < 6; ++d)
     key += "/" + std::to_string(band[d]);
   auto it = cache.tables.find(key);
@@ -737,34 +783,19 @@ int unitOrder(UnitOrderCache &cache, int bmask, const int *band, int rank, int t
     cudaGetLastError();
     return HG_OK;
   }
-  const int xd = rank - 1;
-  std::vector<int> inner, outer;
-  const long total = long(tiles_x) * tiles_y * nchunks;
-  inner.reserve(size_t(total));
-  for (int c = 0; c < nchunks; ++c)
-    for (int ty = 0; ty < tiles_y; ++ty)
-      for (int tx = 0; tx < tiles_x; ++tx) {
-        int m = 0;
-        if (c * chunk < band[0]) m |= 1;
-        if (std::min((c + 1) * chunk, nz) > nz - band[1]) m |= 2;
-        if (rank == 3 && ty * TY < band[2]) m |= 4;
-        if (rank == 3 && std::min((ty + 1) * TY, ny) > ny - band[3]) m |= 8;
-        if (tx * TX < band[2 * xd]) m |= 1 << (2 * xd);
-        if (std::min((tx + 1) * TX, nx) > nx - band[2 * xd + 1]) m |= 2 << (2 * xd);
-        const int u = (c * tiles_y + ty) * tiles_x + tx;
-        (m & bmask ? outer : inner).push_back(u);
-      }
-  const int nin = int(inner.size());
-  inner.insert(inner.end(), outer.begin(), outer.end());
+  UnitGeom g{bmask, rank, tiles_x, tiles_y, nchunks, TX, TY, chunk, nx, ny, nz, {}};
+  for (int d = 0; d < 6; ++d)
+    g.band[d] = band[d];
+  const int total = tiles_x * tiles_y * nchunks;
+  int nin = 0; // the split launch needs the interior count on the host
+  for (int u = 0; u < total; ++u)
+    nin += unitTouches(g, u) ? 0 : 1;
   int *d = nullptr;
-  if (cudaMalloc(&d, inner.size() * sizeof(int)) != cudaSuccess)
-    return cudaErr(cudaGetLastError(), "cudaMalloc(unit order)");
-  const cudaError_t e =
-      cudaMemcpy(d, inner.data(), inner.size() * sizeof(int), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) {
-    cudaFree(d);
-    return cudaErr(e, "cudaMemcpy(unit order)");
-  }
+  if (cudaMallocAsync(&d, size_t(total) * sizeof(int), st) != cudaSuccess)
+    return cudaErr(cudaGetLastError(), "cudaMallocAsync(unit order)");
+  unitOrderKernel<<<1, 1024, 0, st>>>(d, total, nin, g);
+  if (int rc = cudaErr(cudaGetLastError(), "unit order kernel launch"))
+    return rc;
   cache.tables[key] = d;
   cache.inner[key] = nin;
   *perm = d;
@@ -1267,6 +1298,26 @@ __global__ void packKernel(T *base, const DevLayout L, int64_t a0, int64_t a1, i
   }
 }
 
+// A packed x-face slab into its receive box (the order putKernel's packed jobs and the fused
+// send write: [y][z][x] of the box for rank 3, [z][x] for rank 2).
+template <typename T>
+__global__ void slabUnpackKernel(T *base, const DevLayout L, int64_t a0, int64_t a1, int64_t a2,
+                                 int64_t s0, int64_t s1, int64_t s2, const T *slab) {
+  const int64_t total = s0 * s1 * s2;
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total;
+       o += int64_t(gridDim.x) * blockDim.x) {
+    int64_t e;
+    if (L.rank == 3) { // o = (i1 * s0 + i0) * s2 + i2
+      const int64_t i2 = o % s2, q = o / s2, i0 = q % s0, i1 = q / s0;
+      e = ((a0 + i0) * L.shape[1] + (a1 + i1)) * L.pitch + L.col0 + a2 + i2;
+    } else { // o = i0 * s1 + i1
+      const int64_t i1 = o % s1, i0 = o / s1;
+      e = (a0 + i0) * L.pitch + L.col0 + a1 + i1;
+    }
+    base[e] = slab[o];
+  }
+}
+
 struct PutParams {
   PutJob jobs[96];
   int njobs;
@@ -1659,6 +1710,29 @@ int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const 
                                                  unpack);
   }
   return cudaErr(cudaGetLastError(), "pack kernel launch");
+}
+
+int launchSlabUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,
+                     const void *slab, cudaStream_t st) {
+  int64_t a[3] = {0, 0, 0}, s[3] = {1, 1, 1};
+  for (int d = 0; d < lay.rank; ++d) {
+    a[d] = at[d];
+    s[d] = size[d];
+  }
+  const int64_t total = s[0] * s[1] * s[2];
+  if (total <= 0)
+    return HG_OK;
+  const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256,
+                                                                          148 * 16)));
+  if (lay.es == 4)
+    slabUnpackKernel<float><<<blocks, 256, 0, st>>>(static_cast<float *>(base), lay, a[0], a[1],
+                                                    a[2], s[0], s[1], s[2],
+                                                    static_cast<const float *>(slab));
+  else
+    slabUnpackKernel<double><<<blocks, 256, 0, st>>>(static_cast<double *>(base), lay, a[0],
+                                                     a[1], a[2], s[0], s[1], s[2],
+                                                     static_cast<const double *>(slab));
+  return cudaErr(cudaGetLastError(), "slab unpack kernel launch");
 }
 
 int launchPut(const PutJob *jobs, int njobs, const PutSignal *sig, int nsig,

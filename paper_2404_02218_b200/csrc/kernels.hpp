@@ -151,6 +151,9 @@ int launchCopyBox(const void *src, const DevLayout &sl, void *dst, const DevLayo
 // is not moved (both NULL: move everything)
 int launchHostXfer(void *dev, const DevLayout &lay, void *host_dev, int up, const int64_t *skip_lo,
                    const int64_t *skip_hi, cudaStream_t st);
+// packed x-face slab ([y][z][x] box order for rank 3, [z][x] for rank 2) -> the box at `at`
+int launchSlabUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,
+                     const void *slab, cudaStream_t st);
 // box copy between a layout box and a packed array (dir 0 = pack, 1 = unpack)
 int launchPackUnpack(void *base, const DevLayout &lay, const int64_t *at, const int64_t *size,
                      void *packed, int unpack, cudaStream_t st);

@@ -203,8 +203,7 @@ bool compileMultiJit(hg_plan &p, int device, int &st) {
   for (int t = 0; t < g.ntemps; ++t) {
     if (!consumers[static_cast<size_t>(t)] && !stores[static_cast<size_t>(t)])
       continue;
-    st = cudaCheck(cudaMalloc(&p.tmpPtr[static_cast<size_t>(t)], p.lay[0].bytes()),
-                   "cudaMalloc(temp)");
+    st = planAlloc(p, &p.tmpPtr[static_cast<size_t>(t)], p.lay[0].bytes(), "cudaMalloc(temp)");
     if (st)
       return true;
     cudaMemset(p.tmpPtr[static_cast<size_t>(t)], 0, p.lay[0].bytes());
@@ -246,8 +245,7 @@ int compileMulti(hg_plan &p) {
       const int t = A.result_temp[k];
       Layout L = makeLayout(A.domain, g.rank, es, A.domain.lb[g.rank - 1]);
       p.tmpLay[static_cast<size_t>(t)] = L;
-      int st = cudaCheck(cudaMalloc(&p.tmpPtr[static_cast<size_t>(t)], L.bytes()),
-                         "cudaMalloc(temp)");
+      int st = planAlloc(p, &p.tmpPtr[static_cast<size_t>(t)], L.bytes(), "cudaMalloc(temp)");
       if (st)
         return st;
       cudaMemset(p.tmpPtr[static_cast<size_t>(t)], 0, L.bytes());
@@ -351,6 +349,39 @@ int multiStep(hg_plan &p, cudaStream_t st) {
 }
 
 } // namespace
+
+constexpr unsigned char kGuardByte = 0xA5;
+
+int planAlloc(hg_plan &p, void **ptr, size_t bytes, const char *what) {
+  *ptr = nullptr;
+  if (!p.knobs.guards)
+    return cudaCheck(cudaMalloc(ptr, bytes), what);
+  p.guardBytes = 64 << 10;
+  char *base = nullptr;
+  if (int st = cudaCheck(cudaMalloc(&base, bytes + 2 * p.guardBytes), what))
+    return st;
+  if (int st = cudaCheck(cudaMemset(base, kGuardByte, bytes + 2 * p.guardBytes),
+                         "cudaMemset(guards)"))
+    return st;
+  *ptr = base + p.guardBytes;
+  p.guardBase[*ptr] = {base, bytes};
+  return HG_OK;
+}
+
+void planFree(hg_plan &p, void *ptr) {
+  auto it = p.guardBase.find(ptr);
+  if (it == p.guardBase.end()) {
+    cudaFree(ptr);
+    return;
+  }
+  cudaFree(it->second.first);
+  p.guardBase.erase(it);
+}
+
+void *planAllocBase(const hg_plan &p, void *ptr) {
+  auto it = p.guardBase.find(ptr);
+  return it == p.guardBase.end() ? ptr : it->second.first;
+}
 
 int planStep(hg_plan &p, cudaStream_t st) {
   const hg_program &g = p.prog;
@@ -568,7 +599,7 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
   for (int f = 0; f < g.nfields; ++f) {
     Layout L = makeLayout(g.fields[f], g.rank, es, coreLast);
     void *ptr = nullptr;
-    st = cudaCheck(cudaMalloc(&ptr, L.bytes()), "cudaMalloc(field)");
+    st = planAlloc(*p, &ptr, L.bytes(), "cudaMalloc(field)");
     if (st)
       return st;
     p->lay.push_back(L);
@@ -650,12 +681,12 @@ int hg_plan_destroy(hg_plan *p) {
   for (auto &g : p->graphs)
     cudaGraphExecDestroy(g.second);
   for (void *d : p->dptr)
-    cudaFree(d);
+    planFree(*p, d);
   for (void *d : p->shadow)
     if (d)
-      cudaFree(d);
+      planFree(*p, d);
   for (void *d : p->tmpPtr)
-    cudaFree(d);
+    planFree(*p, d);
   if (p->resXbuf)
     cudaFree(p->resXbuf);
   if (p->resFlags)
@@ -665,6 +696,37 @@ int hg_plan_destroy(hg_plan *p) {
   if (p->gopsDev)
     cudaFree(p->gopsDev);
   delete p;
+  return HG_OK;
+}
+
+int hg_plan_check_guards(hg_plan *p) {
+  if (!p)
+    return setError(HG_EINVAL, "null plan");
+  if (p->guardBase.empty())
+    return HG_OK;
+  if (int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice"))
+    return st;
+  if (int st = cudaCheck(cudaDeviceSynchronize(), "cudaDeviceSynchronize"))
+    return st;
+  std::vector<unsigned char> h(p->guardBytes);
+  for (const auto &kv : p->guardBase) {
+    const char *user = static_cast<const char *>(kv.first);
+    const char *base = static_cast<const char *>(kv.second.first);
+    const size_t bytes = kv.second.second;
+    for (int side = 0; side < 2; ++side) {
+      const char *g = side == 0 ? base : user + bytes;
+      if (int st = cudaCheck(cudaMemcpy(h.data(), g, h.size(), cudaMemcpyDeviceToHost),
+                             "cudaMemcpy(guard)"))
+        return st;
+      for (size_t i = 0; i < h.size(); ++i)
+        if (h[i] != kGuardByte)
+          return setError(HG_ETRAP, std::string("out-of-bounds write: guard band ") +
+                                        (side == 0 ? "before" : "after") +
+                                        " a device buffer of " + std::to_string(bytes) +
+                                        " bytes modified at byte " + std::to_string(i) +
+                                        " of the band");
+    }
+  }
   return HG_OK;
 }
 
@@ -1069,7 +1131,7 @@ int ensureShadow(hg_plan &p, int b, cudaStream_t s) {
   uint32_t box[3];
   tbBox(p.an.star, p.prog.dtype, box);
   if (!p.shadow[bi]) {
-    int st = cudaCheck(cudaMalloc(&p.shadow[bi], L.bytes()), "cudaMalloc(shadow)");
+    int st = planAlloc(p, &p.shadow[bi], L.bytes(), "cudaMalloc(shadow)");
     if (st)
       return st;
     p.shadowOk[bi] = 0;

@@ -50,6 +50,10 @@ struct hg_plan {
   int xbox[6] = {0, 0, 0, 0, 0, 0}; // oz, oy, bz, by, ox_lo, ox_hi (xboxSet)
   bool xboxSet = false;
   hg::UnitOrderCache order;           // star launch orders (boundary units last)
+  // HG_DEBUG_GUARDS: guarded allocations (user pointer -> allocation base); 0-byte guards
+  // otherwise
+  std::map<void *, std::pair<void *, size_t>> guardBase; // -> (base, buffer bytes)
+  size_t guardBytes = 0;
   std::shared_ptr<hg::JitKernel> jit;  // fused-apply family (generated, per program)
   std::vector<CUtensorMap> tmApply;   // per buffer, for the fused-apply boxes
   std::map<int, cudaGraphExec_t> graphs; // hg_plan_run: captured G-step graphs per phase
@@ -90,6 +94,11 @@ struct hg_plan {
 
 namespace hg {
 int cudaCheck(cudaError_t e, const char *what);
+// Device allocation of a plan buffer: with knobs.guards, inside canary bands of guardBytes.
+int planAlloc(hg_plan &p, void **ptr, size_t bytes, const char *what);
+void planFree(hg_plan &p, void *ptr);
+// The allocation base and guard offset of a plan buffer (IPC handles need the base).
+void *planAllocBase(const hg_plan &p, void *ptr);
 // One time step on `st` with the current binding, then rotate.
 int planStep(hg_plan &p, cudaStream_t st);
 // Whether hg_plan_run advances this plan by two-step passes (tb.cu).

@@ -443,6 +443,7 @@ Knobs readKnobs() {
   k.tb = on("HG_TB");
   k.starGeo = num("HG_STAR_GEO", -1);
   k.jitDepth = std::max(0, num("HG_JIT_DEPTH", 0));
+  k.guards = on("HG_DEBUG_GUARDS");
   return k;
 }
 
