@@ -105,9 +105,15 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
   int done = 0, blk = 0;
   while (done < P.steps) {
     const int kk = min(P.K, P.steps - done);
+    // f32: the last sub-step before an exchange stores its boundary rows' values straight
+    // into my exchange slot as tagged words while it computes them (no separate copy pass)
     using W64 = unsigned long long;
+    const bool xchNext = sizeof(T) == 4 && done + kk < P.steps;
+    W64 *const mineX = reinterpret_cast<W64 *>(P.xbuf) +
+                       (size_t(blk & 1) * G + c) * 2 * (size_t(E) * P.nx);
     const W64 tagX = W64(P.tag0 + unsigned(blk) + 1u) << 32;
     for (int s = 0; s < kk; ++s) {
+      const bool xch = xchNext && s == kk - 1;
       const int ylo = max(0, r0 - (kk - 1 - s) * R), yhi = min(P.ny, r1 + (kk - 1 - s) * R);
       const T *in = cur ? tile1 : tile0;
       T *out = cur ? tile0 : tile1;
@@ -161,10 +167,38 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
               if (x0 + j < P.nx)
                 dst[j] = o.v[j];
           }
-
+          if constexpr (sizeof(T) == 4) {
+            if (xch) {
+              // slot rows: [0, E) = my first E rows, [E, 2E) = my last E rows (a row can be
+              // both in a band of fewer than 2E rows)
+              const int yy = y + h;
+              for (int side = 0; side < 2; ++side) {
+                const int r = side == 0 ? yy - r0 : E + yy - (r1 - E);
+                if (side == 0 ? yy - r0 >= E : yy < r1 - E)
+                  continue;
+                W64 *m = mineX + size_t(r) * P.nx + x0;
+                if (x0 + 4 <= P.nx) {
+                  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(m),
+                               "l"(tagX | __float_as_uint(o.v[0])),
+                               "l"(tagX | __float_as_uint(o.v[1])));
+                  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(m + 2),
+                               "l"(tagX | __float_as_uint(o.v[2])),
+                               "l"(tagX | __float_as_uint(o.v[3])));
+                } else {
+                  for (int j = 0; j < 4; ++j)
+                    if (x0 + j < P.nx)
+                      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(m + j),
+                                   "l"(tagX | __float_as_uint(o.v[j])));
+                }
+              }
+            }
+          }
         }
       }
-      __syncthreads();
+      // (before an exchange the halo rows the poll below writes are not read by this
+      // sub-step, and its boundary values already went out: the poll needs no barrier first)
+      if (!xch)
+        __syncthreads();
       cur ^= 1;
     }
     done += kk;
@@ -182,19 +216,6 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
       const W64 tg = tagX;
       T *tw = cur ? tile1 : tile0;
       const int nx = P.nx;
-      W64 *mine = xw + (size_t(par) * G + c) * 2 * slot;
-      // my E first and E last rows of the current level, one tagged word per value
-      for (int x = tid; x < nx; x += NTH) {
-        W64 *m = mine + x;
-        const T *sp = tw + rowBase + x;
-#pragma unroll 4
-        for (int r = 0; r < 2 * E; ++r) {
-          const int y = r < E ? r0 + r : r1 - 2 * E + r;
-          const W64 w = tg | __float_as_uint(sp[y * SP]);
-          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(m + size_t(r) * nx), "l"(w)
-                       : "memory");
-        }
-      }
       // the neighbours' rows: row r of my 2E halo rows (r < E: above, from the upper band's
       // last E rows; else below, from the lower band's first E rows)
       const W64 *above = xw + (size_t(par) * G + (c - 1)) * 2 * slot + slot;
