@@ -489,9 +489,11 @@ def run_ours(args):
     peak, peak_src = _peaks()
     bpp = WORKLOADS[args.workload]["bpp"]
     achieved = bpp * core_local / (k_ms / 1e3) / 1e9
-    traffic = _ncu_traffic({"heat3d_weak": "r1_heat3d_so4_1024", "pw_advection": "r1_pw_advection_128x512x512",
-                            "wave3d_1024": "r1_wave3d_so8_1024",
-                            "heat2d_1024": "r1_resident_heat2d_1024"}.get(args.workload, ""))
+    traffic = _ncu_traffic({"heat3d_weak": "r2_heat3d_so4_1024",
+                            "heat3d_512": "r2_heat3d_so4_512",
+                            "pw_advection": "r2_pw_advection_128x512x512",
+                            "wave3d_1024": "r2_wave3d_so8_1024",
+                            "heat2d_1024": "r2_resident_heat2d_1024"}.get(args.workload, ""))
 
     # end to end through the public API with HOST buffers: upload -> T steps -> download
     e2e = None

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
                 if (side == 0 ? yy - r0 >= E : yy < r1 - E)
                   continue;
                 W64 *m = mineX + size_t(r) * P.nx + x0;
-                if (x0 + 4 <= P.nx) {
+                if (x0 + 4 <= P.nx && (reinterpret_cast<uintptr_t>(m) & 15) == 0) {
                   asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(m),
                                "l"(tagX | __float_as_uint(o.v[0])),
                                "l"(tagX | __float_as_uint(o.v[1])));
