@@ -881,6 +881,15 @@ int hg_dmp_create_ex(hg_plan *plan, const hg_decomp *dc, int64_t rank, const hg_
       // width only -- enough for depth 2 alone
       if (plan->an.star.kind == kWave && d->depth > 2)
         return setError(HG_EUNSUPPORTED, "deep halos of a prev/cur/next step support depth 2");
+      // the extended region of a round's first steps reaches the corners between two split
+      // dims (e.g. the z band over the y halo), which face exchanges do not carry
+      int split = 0;
+      for (int q = 0; q < dc->ndim; ++q)
+        split += dc->grid[q] > 1 ? 1 : 0;
+      if (split > 1)
+        return setError(HG_EUNSUPPORTED, "deep halos need a grid that splits one dimension "
+                                         "(the extended region would read corner cells that "
+                                         "face exchanges do not carry)");
       for (int s = 0; s < dc->nswaps; ++s)
         for (int k = 0; k < dc->swaps[s].nexchanges; ++k) {
           const hg_exchange &e = dc->swaps[s].ex[k];
