@@ -54,6 +54,7 @@ struct Knobs {
   bool tb = false;            // HG_TB=1: two-step passes for large 3D heat (opt-in)
   int starGeo = -1;           // HG_STAR_GEO=n: force the star tile geometry
   int jitDepth = 0;           // HG_JIT_DEPTH=n: TMA ring depth of the fused-apply family
+  int pitchPad = 0;           // HG_PITCH_PAD=n: n extra 128-byte lines per row (layout A/B)
   bool guards = false;        // HG_DEBUG_GUARDS=1: canary bands around every device buffer of
                               // the plan (hg_plan_check_guards finds out-of-bounds writes)
 };
@@ -82,7 +83,9 @@ struct Layout {
     return n;
   }
 };
-Layout makeLayout(const hg_bounds &b, int rank, int es, int64_t core_lb_last);
+// padLines: extra 128-byte lines per row (HG_PITCH_PAD experiments)
+Layout makeLayout(const hg_bounds &b, int rank, int es, int64_t core_lb_last,
+                  int padLines = 0);
 
 // ---- generic (bytecode) program for the generic kernel ---------------------------------
 struct GOp {       // compact, slot-allocated

@@ -1495,9 +1495,10 @@ int makeBoxTensorMap(int dtype, const DevLayout &lay, void *base, const uint32_t
 }
 
 int starGeoFor(const StarSpec &s, int dtype, int rank, const int64_t *ext) {
-  // wide tiles pay on large planes (>= 768 x 768); 512^2 planes prefer the 64 x 16 tile
-  return rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2 && ext[1] >= 768 &&
-                 ext[2] >= 768
+  // the wide 128 x 12 tile wins on every plane of at least 256 x 64 (tools/geo_ab.py, round 2:
+  // +2% at 512^3, +9% on 2048 x 2048 x 512, +15% on 2048 x 512 x 2048); tiny planes keep 64 x 16
+  return rank == 3 && dtype == HG_F32 && s.kind == kHeat && s.ntaps <= 2 && ext[1] >= 64 &&
+                 ext[2] >= 256
              ? 1
              : 0;
 }

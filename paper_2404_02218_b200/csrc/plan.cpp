@@ -597,7 +597,7 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
   const int es = g.dtype == HG_F32 ? 4 : 8;
   const int64_t coreLast = storedRegion(g, 0).lb[g.rank - 1];
   for (int f = 0; f < g.nfields; ++f) {
-    Layout L = makeLayout(g.fields[f], g.rank, es, coreLast);
+    Layout L = makeLayout(g.fields[f], g.rank, es, coreLast, p->knobs.pitchPad);
     void *ptr = nullptr;
     st = planAlloc(*p, &ptr, L.bytes(), "cudaMalloc(field)");
     if (st)

@@ -37,7 +37,7 @@ uint64_t fnv1a(const void *p, size_t n) {
   return h;
 }
 
-Layout makeLayout(const hg_bounds &b, int rank, int es, int64_t core_lb_last) {
+Layout makeLayout(const hg_bounds &b, int rank, int es, int64_t core_lb_last, int padLines) {
   // Reference layout is row-major with the last dim fastest (buffer.cpp:65-70).  On the
   // device each row of the last dim is padded to a 128-byte pitch and shifted so that the
   // first core element of a row starts a 128-byte line (coalesced, TMA-legal strides).
@@ -54,7 +54,7 @@ Layout makeLayout(const hg_bounds &b, int rank, int es, int64_t core_lb_last) {
   if (j0 < 0 || j0 >= S)
     j0 = 0;
   L.col0 = va * ((j0 + 8 + va - 1) / va) - j0;
-  L.pitch = ((L.col0 + S + va - 1) / va) * va;
+  L.pitch = ((L.col0 + S + va - 1) / va + std::max(padLines, 0)) * va;
   L.rows = 1;
   for (int d = 0; d < rank - 1; ++d)
     L.rows *= L.shape[d];
@@ -444,6 +444,7 @@ Knobs readKnobs() {
   k.starGeo = num("HG_STAR_GEO", -1);
   k.jitDepth = std::max(0, num("HG_JIT_DEPTH", 0));
   k.guards = on("HG_DEBUG_GUARDS");
+  k.pitchPad = std::max(0, num("HG_PITCH_PAD", 0));
   return k;
 }
 
