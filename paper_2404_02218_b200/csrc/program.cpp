@@ -54,7 +54,15 @@ Layout makeLayout(const hg_bounds &b, int rank, int es, int64_t core_lb_last, in
   if (j0 < 0 || j0 >= S)
     j0 = 0;
   L.col0 = va * ((j0 + 8 + va - 1) / va) - j0;
-  L.pitch = ((L.col0 + S + va - 1) / va + std::max(padLines, 0)) * va;
+  int64_t lines = (L.col0 + S + va - 1) / va;
+  // Row strides of a multiple of 17 lines of 128 B (1088 floats, 1632, 2176, ...) make the
+  // star kernel's concurrent plane reads collide in the memory system: heat SDO4 1024^3 runs
+  // at 705 GPts/s with 34 lines per row and 752-758 with 35 or 36, and the 51- and 68-line
+  // rows lose 4-7% the same way, while 33/35/36/50/52/66 are all fine (tools/pitch_ab2.py,
+  // profiles/r2_pitch.md).  One more line breaks the period.
+  if (lines % 17 == 0)
+    ++lines;
+  L.pitch = (lines + std::max(padLines, 0)) * va;
   L.rows = 1;
   for (int d = 0; d < rank - 1; ++d)
     L.rows *= L.shape[d];
