@@ -266,70 +266,73 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     need &= P.wmask;
   }
   // packed x faces: the slab rows this unit's boxes read (its rows and y rim, its planes and
-  // z rim, clipped to the receive box) are unpacked into the halo columns by the whole CTA
-  // (many loads in flight), after the wait and before any TMA load
+  // z rim, clipped to the receive box) are unpacked into the halo columns by the producer warp,
+  // a batch of planes at a time just ahead of the TMA loads that read them, so the consumers
+  // start at once and the unpack overlaps their work
   const int xunpack = (need >> (2 * (RANK - 1))) & ((P.xin[0] ? 1 : 0) | (P.xin[1] ? 2 : 0));
-  if (xunpack) {
-    if (tid == 0)
-      for (int di = 0; di < 6; ++di)
-        if (need & (1 << di))
-          waitFlag(P.flags + di, P.epoch, P.err, P.timeout_ns,
-                   (P.epoch << 8) | (unsigned long long)(di << 1) | 1ull);
-    __syncthreads();
-#pragma unroll 1
-    for (int sd = 0; sd < 2; ++sd) {
-      if (!(xunpack & (1 << sd)))
-        continue;
-      const T *slab = P.xin[sd];
-      const int W = P.xw[sd];
-      const int y0 = RANK == 3 ? max(P.xoy, yb - RY) : 0;
-      const int y1 = RANK == 3 ? min(P.xoy + P.xby, yb + C::TY + RY) : 1;
-      const int z0 = max(P.xoz, zb - R), z1 = min(P.xoz + P.xbz, zb + n + R);
-      const int per = (z1 - z0) * W;
-      const int total = (y1 - y0) * per;
-      const T *src0 = slab + (int64_t(y0 - P.xoy) * P.xbz + (z0 - P.xoz)) * W;
-      const int64_t rowStride = int64_t(P.xbz) * W;
-      T *dst0 = P.cur + int64_t(P.zs + z0) * P.plane +
-                (RANK == 3 ? int64_t(P.ys + y0) * P.pitch : 0) + P.col0 + P.xs + P.xox[sd];
-      constexpr int B = 4; // independent loads in flight per thread
-      for (int k0 = tid; k0 < total; k0 += B * C::NTHREADS) {
-        T v[B];
-        int64_t o[B];
-#pragma unroll
-        for (int j = 0; j < B; ++j) {
-          const int k = k0 + j * C::NTHREADS;
-          if (k < total) {
-            const int row = k / per, kk = k - row * per, dz = kk / W;
-            v[j] = src0[row * rowStride + kk];
-            o[j] = (RANK == 3 ? int64_t(row) * P.pitch : 0) + int64_t(dz) * P.plane +
-                   (kk - dz * W);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < B; ++j)
-          if (k0 + j * C::NTHREADS < total)
-            dst0[o[j]] = v[j];
-      }
-    }
-    // the halo bytes arrived through the generic proxy; TMA reads via the async proxy
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncthreads();
-  }
 
   if (tid >= C::NCONS) {
     // ---------------- producer warp ----------------
     const int plane_lane = tid - C::NCONS;
-    if (need && !xunpack && plane_lane == 0) {
-      for (int di = 0; di < 6; ++di)
-        if (need & (1 << di))
-          waitFlag(P.flags + di, P.epoch, P.err, P.timeout_ns,
-                   (P.epoch << 8) | (unsigned long long)(di << 1) | 1ull);
+    if (need) {
+      if (plane_lane == 0)
+        for (int di = 0; di < 6; ++di)
+          if (need & (1 << di))
+            waitFlag(P.flags + di, P.epoch, P.err, P.timeout_ns,
+                     (P.epoch << 8) | (unsigned long long)(di << 1) | 1ull);
       // the halo bytes arrived through the generic proxy; TMA reads via the async proxy
       asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
     }
-    if (plane_lane == 0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur))
-                   : "memory");
+    // x unpack geometry: rows [uy0, uy1), planes [uz0, uz1) of the region (clipped to the box)
+    const int uy0 = RANK == 3 ? max(P.xoy, yb - RY) : 0;
+    const int uy1 = RANK == 3 ? min(P.xoy + P.xby, yb + C::TY + RY) : 1;
+    const int uz0 = max(P.xoz, zb - R), uz1 = min(P.xoz + P.xbz, zb + n + R);
+    int unpacked = xunpack ? uz0 : 1 << 30; // planes below this z (region) are in place
+    // unpack planes [unpacked, zEnd) of both x faces with the whole warp, then proxy-fence
+    auto unpackTo = [&](int zEnd) {
+      zEnd = min(zEnd, uz1);
+      if (unpacked >= zEnd)
+        return;
+#pragma unroll 1
+      for (int sd = 0; sd < 2; ++sd) {
+        if (!(xunpack & (1 << sd)))
+          continue;
+        const int W = P.xw[sd];
+        const int per = (zEnd - unpacked) * W, total = (uy1 - uy0) * per;
+        const T *src0 = P.xin[sd] + (int64_t(uy0 - P.xoy) * P.xbz + (unpacked - P.xoz)) * W;
+        const int64_t rowStride = int64_t(P.xbz) * W;
+        T *dst0 = P.cur + int64_t(P.zs + unpacked) * P.plane +
+                  (RANK == 3 ? int64_t(P.ys + uy0) * P.pitch : 0) + P.col0 + P.xs + P.xox[sd];
+        constexpr int B = 8; // independent loads in flight per lane
+        for (int k0 = plane_lane; k0 < total; k0 += B * 32) {
+          T v[B];
+          int64_t o[B];
+#pragma unroll
+          for (int j = 0; j < B; ++j) {
+            const int k = k0 + j * 32;
+            if (k < total) {
+              const int row = k / per, kk = k - row * per, dz = kk / W;
+              v[j] = src0[row * rowStride + kk];
+              o[j] = (RANK == 3 ? int64_t(row) * P.pitch : 0) + int64_t(dz) * P.plane +
+                     (kk - dz * W);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < B; ++j)
+            if (k0 + j * 32 < total)
+              dst0[o[j]] = v[j];
+        }
+      }
+      unpacked = zEnd;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
+    };
+    // with x unpacking the whole warp walks the plane loop; lane 0 issues barriers and TMA
+    if (plane_lane == 0 || xunpack) {
+      if (plane_lane == 0)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmCur))
+                     : "memory");
       const int cx = int(P.col0) + P.xs + xb - C::PADX;
       const int cy = RANK == 3 ? P.ys + yb - RY : 0;
       const int z0 = P.zs + zb - R;
@@ -347,8 +350,13 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       // slot p holds planes p*ZP .. p*ZP+ZP-1 (plane i is z = z0 + i); a plane past the
       // field's end is zero-filled by TMA and never read
       const int nslots = (n + 2 * R + ZP - 1) / ZP;
+      constexpr int UNPACK_PLANES = 8; // x unpack batch, ahead of the TMA loads
       for (int p = 0; p < nslots; ++p) {
         const int s = p % NS, i = p * ZP;
+        if (xunpack && zb - R + i + ZP > unpacked) // planes z0+i.. need their halo columns
+          unpackTo(zb - R + i + ZP + UNPACK_PLANES);
+        if (plane_lane != 0)
+          continue;
         if (p >= NS)
           mbarWait(&empty[s], uint32_t((p / NS - 1) & 1));
         const bool wantPrev = C::WAVE && i + ZP - 1 >= R && i < n + R;
