@@ -123,6 +123,10 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
 #ifndef HG_ZP
 #define HG_ZP 1
 #endif
+// compile-time 10-slot ring on the 128x12 tile too (A/B variant builds only)
+#ifndef HG_GEO1_CT
+#define HG_GEO1_CT 0
+#endif
 // L2 eviction hints on the z-halo planes shared by consecutive chunks (A/B: HG_L2HINT=0)
 #ifndef HG_L2HINT
 #define HG_L2HINT 1
@@ -197,7 +201,7 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   // heat 512^3 +4%).  The wide 128x12 tile keeps the 8-slot ring: at 10 slots its DRAM reads
   // grew 5% (ncu: 4.76 -> 5.01 GB per 1024^3 step) and it ran 4% slower (A/B on one box).
   static constexpr int DEPTH =
-      RANK == 3 ? (R <= 2 ? (sizeof(T) == 4 && HG_ZP == 1 && GEO == 0 ? 7 : HG_DEPTH3)
+      RANK == 3 ? (R <= 2 ? (sizeof(T) == 4 && HG_ZP == 1 && (GEO == 0 || HG_GEO1_CT) ? 7 : HG_DEPTH3)
                           : (sizeof(T) == 8 ? 5 : HG_DEPTH3W))
                 : HG_DEPTH2;
   static constexpr int ZP = HG_ZP;                  // planes per ring slot
