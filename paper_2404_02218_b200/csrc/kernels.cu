@@ -123,9 +123,10 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
 #ifndef HG_ZP
 #define HG_ZP 1
 #endif
-// compile-time 10-slot ring on the 128x12 tile too (A/B variant builds only)
+// compile-time 10-slot ring on the 128x12 tile too: rejected before the 35-line pitch (its DRAM
+// reads grew 5%), +4% on two boxes after it (profiles/r2_ab.md)
 #ifndef HG_GEO1_CT
-#define HG_GEO1_CT 0
+#define HG_GEO1_CT 1
 #endif
 // L2 eviction hints on the z-halo planes shared by consecutive chunks (A/B: HG_L2HINT=0)
 #ifndef HG_L2HINT
@@ -196,10 +197,9 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int MINB =
       GEO == 1 ? 2 : GEO == 2 ? HG_MINB_G2
                    : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
-  // f32 3D radius <= 2 on the 64x16 tile: the ring is 2Q (heat SDO4) / 3Q (SDO2) slots deep,
-  // so the plane loop unrolled over one ring turn has compile-time slot indices (StarCfg::CT;
-  // heat 512^3 +4%).  The wide 128x12 tile keeps the 8-slot ring: at 10 slots its DRAM reads
-  // grew 5% (ncu: 4.76 -> 5.01 GB per 1024^3 step) and it ran 4% slower (A/B on one box).
+  // f32 3D radius <= 2: the ring is 2Q (heat SDO4) / 3Q (SDO2) slots deep, so the plane loop
+  // unrolled over one ring turn has compile-time slot indices (StarCfg::CT; 18% fewer
+  // instructions per point on the 128x12 tile, +4% on heat SDO4 1024^3 and 512^3)
   static constexpr int DEPTH =
       RANK == 3 ? (R <= 2 ? (sizeof(T) == 4 && HG_ZP == 1 && (GEO == 0 || HG_GEO1_CT) ? 7 : HG_DEPTH3)
                           : (sizeof(T) == 8 ? 5 : HG_DEPTH3W))
