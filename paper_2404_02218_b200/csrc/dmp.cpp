@@ -442,9 +442,7 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
         waited = true;
       }
       // my receive box on that face: the `at` of my exchange toward the sender
-      int64_t at[3];
-      for (int q = 0; q < 3; ++q)
-        at[q] = x.recv_at[q]; // same template both ways (mate's at == my at for my face)
+      int64_t at[3] = {0, 0, 0};
       const hg_swap &sw0 = d.dc.swaps[x.swap];
       for (int k = 0; k < sw0.nexchanges; ++k) {
         int dim2, sign2;
@@ -460,7 +458,6 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
       ++p.launches;
     }
   }
-  const bool packedRound = d.xpack;
   // 2. the stencil step; halo-reading CTAs wait for the round in-kernel
   if (star && nw) {
     p.waitFlags = d.flags;
@@ -474,7 +471,7 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     }
     for (int di = 0; di < kDirs; ++di)
       p.band[di] = band[di];
-    if (d.xpack && ph == 0 && packedRound) { // the cur buffer's x halo arrives packed
+    if (d.xpack && ph == 0) { // the cur buffer's x halo arrives packed (every data round)
       const int xd = g.rank - 1;
       const int bCur =
           p.bind[static_cast<size_t>(g.operand_field[p.an.star.cur_operand])];
