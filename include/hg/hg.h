@@ -31,11 +31,17 @@
  *   hg_decompose_program ....... the `decompose` pass on a step program  dmp_transforms.cpp:101-312
  *   hg_plan_pack/unpack ........ packRegion/unpackRegion                 simulator.cpp:523-584
  *   hg_dmp_* ................... RankHooks::swap + Endpoint/Transport    simulator.cpp:772-834,
- *                                transport.cpp:13-40: a face-halo exchange of device buffers
- *                                over NVLink peer memory (CUDA IPC between processes, direct
- *                                peer pointers inside one process)
+ *                                201-260, 409-424; transport.cpp:13-40: a face-halo exchange of
+ *                                device buffers, either NVLink stores fused into the stencil
+ *                                kernel (CUDA IPC between processes, peer pointers inside one
+ *                                process; x faces as packed slabs) or NCCL send/recv driven from
+ *                                C++ (hg_dmp_opts.transport); bounded waits report a stuck peer
+ *                                as HG_ETRAP like the reference's deadlock report
+ *                                (simulator.cpp:143-173)
  *   hg_sim_run ................. exec::simulate's per-step loop          simulator.cpp:1066-1203
- *                                (all ranks of one process, event-ordered)
+ *                                (all ranks of one process; one rank per GPU runs the fused
+ *                                protocol, ranks sharing a GPU are event-ordered)
+ *   hg_decompose_program_deep .. beyond the reference: deep (k-step) halos
  *   hg_gpts_per_sec ............ exec::gptsPerSec                        throughput.cpp:19-23
  */
 #ifndef HG_HG_H
