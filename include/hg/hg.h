@@ -286,6 +286,13 @@ int hg_plan_set_tuning(hg_plan *plan, int chunks, int boundary_last);
  * out-of-bounds-write check this pool allows: compute-sanitizer is closed here).  HG_OK
  * without guards. */
 int hg_plan_check_guards(hg_plan *plan);
+/* Caller-bound device memory: buffer `buffer` lives in the caller's allocation
+ * from now on (the plan's own is freed; the caller's is never freed by the plan).  It must be
+ * device memory of the plan's device, 128-byte aligned, at least hg_plan_layout()'s
+ * pitch * rows * elem_bytes bytes, laid out as hg_plan_layout describes (pitched rows, core
+ * on 128-byte lines).  The contents are the caller's: hg_plan_init_fields / upload fill it, or
+ * the caller writes it.  Plans with bound buffers never use the opt-in two-step passes. */
+int hg_plan_bind(hg_plan *plan, int buffer, void *device_ptr, size_t bytes);
 /* Block until all work queued for the plan's device has finished. */
 int hg_plan_synchronize(hg_plan *plan);
 /* Kernel launches issued by this plan so far (for bench/gpu_launches accounting). */

@@ -383,6 +383,10 @@ class Plan:
             finally:
                 lib().hg_plan_destroy(h)
 
+    def bind(self, b: int, device_ptr: int, nbytes: int):
+        """hg_plan_bind: buffer b lives in caller memory (see layout(b) for its shape)."""
+        check(lib().hg_plan_bind(self.h, b, C.c_void_p(device_ptr), nbytes))
+
     def check_guards(self):
         """HG_DEBUG_GUARDS=1 plans: raise HgError(HG_ETRAP) on an out-of-bounds write."""
         check(lib().hg_plan_check_guards(self.h))

@@ -146,6 +146,7 @@ def lib() -> C.CDLL:
         "hg_plan_launch_count": (I64, [V]),
         "hg_plan_synchronize": (C.c_int, [V]),
         "hg_plan_check_guards": (C.c_int, [V]),
+        "hg_plan_bind": (C.c_int, [V, C.c_int, V, SZ]),
         "hg_plan_set_tuning": (C.c_int, [V, C.c_int, C.c_int]),
         "hg_dmp_create": (C.c_int, [V, P(HgDecomp), I64, P(V)]),
         "hg_dmp_create_ex": (C.c_int, [V, P(HgDecomp), I64, P(HgDmpOpts), P(V)]),

@@ -1362,20 +1362,33 @@ template <typename T> __global__ void putKernel(const __grid_constant__ PutParam
   const T *src = static_cast<const T *>(J.src);
   T *dst = static_cast<T *>(J.dst);
   if (J.packed) {
-    // element k of the send box (row-major z, y, x) -> slab [y][z][x]
+    // slab element o ([y][z][x] of the box for rank 3, [z][x] for rank 2) <- its box point;
+    // four consecutive slab elements per thread, stored as one 16-byte NVLink write (a 4-byte
+    // store would cost a whole 32-byte packet each: ncu nvltx 9x the payload)
     const int64_t total = rowsEff * w;
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < total;
-         k += int64_t(gridDim.x) * blockDim.x) {
-      const int64_t i2 = k % w, r = k / w;
-      int64_t i0 = r, i1 = 0, o;
+    auto srcOf = [&](int64_t o) {
+      const int64_t i2 = o % w, q = o / w;
       if (L.rank == 3) {
-        i0 = r / J.size[1];
-        i1 = r % J.size[1];
-        o = (i1 * J.size[0] + i0) * w + i2;
-      } else {
-        o = r * w + i2;
+        const int64_t i0 = q % J.size[0], i1 = q / J.size[0];
+        return boxElem(L, J.src_at, i0, i1, i2);
       }
-      dst[o] = src[L.rank == 3 ? boxElem(L, J.src_at, i0, i1, i2) : boxElem(L, J.src_at, i0, i2, 0)];
+      return boxElem(L, J.src_at, q, i2, 0);
+    };
+    const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    for (int64_t o = 4 * (blockIdx.x * int64_t(blockDim.x) + threadIdx.x); o < total;
+         o += 4 * int64_t(gridDim.x) * blockDim.x) {
+      T v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        v[j] = o + j < total ? src[srcOf(o + j)] : T(0);
+      if (aligned && o + 4 <= total) {
+        st4(dst + o, V4<T>{{v[0], v[1], v[2], v[3]}});
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (o + j < total)
+            dst[o + j] = v[j];
+      }
     }
   } else {
     // 16-byte path when both rows start 16-byte aligned (z/y faces: rows of the core width,

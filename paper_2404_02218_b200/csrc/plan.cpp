@@ -680,8 +680,9 @@ int hg_plan_destroy(hg_plan *p) {
   cudaSetDevice(p->device);
   for (auto &g : p->graphs)
     cudaGraphExecDestroy(g.second);
-  for (void *d : p->dptr)
-    planFree(*p, d);
+  for (size_t b = 0; b < p->dptr.size(); ++b)
+    if (b >= p->callerOwned.size() || !p->callerOwned[b])
+      planFree(*p, p->dptr[b]);
   for (void *d : p->shadow)
     if (d)
       planFree(*p, d);
@@ -1351,6 +1352,54 @@ int hg_plan_unpack(hg_plan *p, int b, const int64_t *at, const int64_t *size, co
 }
 
 int64_t hg_plan_launch_count(const hg_plan *p) { return p ? p->launches : 0; }
+
+int hg_plan_bind(hg_plan *p, int b, void *dptr, size_t bytes) {
+  HG_GUARD_BEGIN
+  if (!p || !dptr || b < 0 || b >= static_cast<int>(p->dptr.size()))
+    return setError(HG_EINVAL, "bad plan/buffer/pointer");
+  const Layout &L = p->lay[static_cast<size_t>(b)];
+  if (bytes < L.bytes())
+    return setError(HG_EINVAL, "bound memory is smaller than the buffer's layout (" +
+                                   std::to_string(L.bytes()) + " bytes; hg_plan_layout)");
+  if (reinterpret_cast<uintptr_t>(dptr) % 128 != 0)
+    return setError(HG_EINVAL, "bound memory must be 128-byte aligned (the layout starts every "
+                               "core row on a 128-byte line)");
+  if (int st = cudaCheck(cudaSetDevice(p->device), "cudaSetDevice"))
+    return st;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, dptr) != cudaSuccess || at.type != cudaMemoryTypeDevice ||
+      at.device != p->device) {
+    cudaGetLastError();
+    return setError(HG_EINVAL, "bound memory must be device memory of the plan's device");
+  }
+  if (int st = cudaCheck(cudaDeviceSynchronize(), "cudaDeviceSynchronize"))
+    return st;
+  const size_t bi = static_cast<size_t>(b);
+  p->callerOwned.resize(p->dptr.size(), 0);
+  if (!p->callerOwned[bi])
+    planFree(*p, p->dptr[bi]);
+  p->dptr[bi] = dptr;
+  p->callerOwned[bi] = 1;
+  p->tbOff = true; // two-step passes swap buffers with plan-owned shadows
+  // every descriptor that captured the old address
+  for (auto &g : p->graphs)
+    cudaGraphExecDestroy(g.second);
+  p->graphs.clear();
+  const hg_program &g = p->prog;
+  if (p->an.family == Family::Star && bi < p->tmCur.size())
+    if (int st = makeStarTensorMaps(p->an.star, g.dtype, g.rank, devLayout(L), dptr,
+                                    &p->tmCur[bi], &p->tmPrev[bi], p->starGeo))
+      return st;
+  if (p->jit && bi < p->tmApply.size())
+    if (int st = jitTensorMap(*p->jit, g.dtype, g.rank, L, dptr, &p->tmApply[bi]))
+      return st;
+  for (auto &M : p->multi)
+    if (M.jit && bi < M.tmField.size())
+      if (int st = jitTensorMap(*M.jit, g.dtype, g.rank, L, dptr, &M.tmField[bi]))
+        return st;
+  return HG_OK;
+  HG_GUARD_END
+}
 
 int hg_plan_synchronize(hg_plan *p) {
   if (!p)

@@ -53,6 +53,7 @@ struct hg_plan {
   // HG_DEBUG_GUARDS: guarded allocations (user pointer -> allocation base); 0-byte guards
   // otherwise
   std::map<void *, std::pair<void *, size_t>> guardBase; // -> (base, buffer bytes)
+  std::vector<char> callerOwned;      // per buffer: bound by hg_plan_bind (never freed by us)
   size_t guardBytes = 0;
   std::shared_ptr<hg::JitKernel> jit;  // fused-apply family (generated, per program)
   std::vector<CUtensorMap> tmApply;   // per buffer, for the fused-apply boxes

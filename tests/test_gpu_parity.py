@@ -561,3 +561,42 @@ def test_live_upload_multi_apply(port):
     assert perm == perm_o
     for g, p in zip(got, perm_o):
         assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
+
+
+@pytest.mark.parametrize("spec,T", [(("heat", 3, 70, 4), 3), (("wave", 3, 40, 8), 4),
+                                    (("heat", 2, 300, 2), 5)])
+def test_caller_bound_device_fields(port, spec, T):
+    # hg_plan_bind: the fields live in the caller's device memory (torch tensors
+    # here, laid out as hg_plan_layout says); init, steps and downloads go through them, and the
+    # caller sees the results in its own tensors without a copy
+    import torch
+    prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
+    arrays = port.initial_fields(prog)
+    perm_o = port.run(prog, arrays, T)
+    plan = hg.Plan(prog)
+    try:
+        owned = []
+        for b in range(prog.nfields):
+            L = plan.layout(b)
+            nbytes = L.pitch * L.rows * L.elem_bytes
+            t = torch.empty(nbytes // 4 + 32, dtype=torch.float32, device="cuda")
+            off = (-t.data_ptr()) % 128 // 4  # 128-byte aligned start inside the tensor
+            owned.append((t, off, L))
+            plan.bind(b, t.data_ptr() + 4 * off, nbytes)
+        plan.init_fields()
+        plan.run(T)
+        perm, _ = plan.binding()
+        got = [plan.download(p) for p in perm]
+        torch.cuda.synchronize()
+        # the caller's own tensor holds the final field (its core rows at col0 of each row)
+        t, off, L = owned[perm[0]]
+        lo, hi = prog.field_bounds(perm[0])
+        shape = [u - l for l, u in zip(lo, hi)]
+        raw = t[off:off + L.pitch * L.rows].view(L.rows, L.pitch)[:, L.col0:L.col0 + shape[-1]]
+        assert np.array_equal(raw.cpu().numpy().reshape(shape).view(np.uint32),
+                              arrays[perm_o[0]].view(np.uint32))
+    finally:
+        plan.close()
+    assert perm == perm_o
+    for g, p in zip(got, perm_o):
+        assert np.array_equal(g.view(np.uint32), arrays[p].view(np.uint32))
