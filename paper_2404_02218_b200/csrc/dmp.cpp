@@ -168,6 +168,10 @@ struct hg_dmp {
   int depth = 1;
   int64_t unit[HG_MAX_RANK] = {0, 0, 0};
   int phase = 0, klen = 1;
+  // deep halos on a grid that splits several dims: the round's exchange runs dim by dim at
+  // the round start, each dim's boxes spanning the halos of the dims exchanged before it, so
+  // the corner cells the extended region reads travel too (stand-alone puts, no fused sends)
+  bool sequenced = false;
 };
 
 namespace hg {
@@ -348,6 +352,83 @@ void deepRegion(const hg_dmp &d, int ph, int kl, int64_t ext[][2], int *band) {
   }
 }
 
+// Deep halos on a grid splitting several dims: the round's exchange at the round start, one
+// split dim after the other (dims in order).  Dim q's boxes span [-W_e, n_e + W_e) in every
+// split dim e < q -- the halo rows that dim e's exchange just filled -- so the corner cells of
+// the extended region arrive from the diagonal ranks through two hops, as an MPI dimension-
+// ordered halo exchange does.  Each dim: a put of the boxes (direct stores), its flag, then a
+// wait for the neighbours' puts of that dim.  The neighbours' last step of the previous round
+// signalled first (their readers of these halos are done).
+int seqRoundStart(hg_dmp &d, bool waitPrev, cudaStream_t st) {
+  hg_plan &p = *d.plan;
+  const int r = p.prog.rank;
+  unsigned long long *err = d.flags + kErr;
+  int all[kDirs], na = 0;
+  for (int di = 0; di < 2 * r; ++di)
+    if (d.nbr[di] >= 0)
+      all[na++] = di;
+  if (waitPrev && na) {
+    if (int rc = launchWaitFlags(d.flags, all, na, d.epoch, err, d.timeoutNs, st))
+      return rc;
+    ++p.launches;
+  }
+  std::vector<Xjob> xs;
+  if (int rc = collectJobs(d, xs))
+    return rc;
+  ++d.epoch; // this round's data epoch (every face word gets it from its dim's put)
+  // halo widths of the split dims (the template's face boxes)
+  int64_t W[HG_MAX_RANK] = {0, 0, 0};
+  for (const Xjob &x : xs)
+    W[x.dim] = std::max(W[x.dim], x.size[x.dim]);
+  for (int q = 0; q < r; ++q) {
+    if (d.dc.grid[q] < 2)
+      continue;
+    std::vector<PutJob> jobs;
+    PutSignal sig[2];
+    int ns = 0, widx[2], nw = 0;
+    for (int sd = 0; sd < 2; ++sd) {
+      const int di = 2 * q + sd;
+      if (d.nbr[di] < 0)
+        continue;
+      sig[ns++].flag = d.peerFlags[di] + (di ^ 1);
+      widx[nw++] = di;
+    }
+    for (const Xjob &x : xs) {
+      if (x.dim != q)
+        continue;
+      PutJob j{};
+      j.src = p.dptr[static_cast<size_t>(x.buffer)];
+      j.dst = d.peer[x.dir][x.buffer];
+      j.lay = devLayout(p.lay[static_cast<size_t>(x.buffer)]);
+      for (int e = 0; e < 3; ++e) {
+        j.src_at[e] = x.send_at[e];
+        j.dst_at[e] = x.recv_at[e];
+        j.size[e] = x.size[e];
+        if (e < q && d.dc.grid[e] > 1) { // span the halos dim e's exchange just filled
+          j.src_at[e] -= W[e];
+          j.dst_at[e] -= W[e];
+          j.size[e] += 2 * W[e];
+        }
+      }
+      int64_t n = 1;
+      for (int e = 0; e < r; ++e)
+        n *= j.size[e];
+      d.bytes += n * p.lay[static_cast<size_t>(x.buffer)].es;
+      jobs.push_back(j);
+    }
+    if (int rc = launchPut(jobs.data(), static_cast<int>(jobs.size()), sig, ns, d.epoch,
+                           d.counter, st))
+      return rc;
+    ++p.launches;
+    if (nw) {
+      if (int rc = launchWaitFlags(d.flags, widx, nw, d.epoch, err, d.timeoutNs, st))
+        return rc;
+      ++p.launches;
+    }
+  }
+  return HG_OK;
+}
+
 // One time step of this rank on the flag (P2P) protocol: [ready handshake], stand-alone put
 // of what the previous step did not fuse, the stencil (halo-reading units wait in-kernel),
 // with the NEXT step's swap of the output fused into it unless this is the call's last step.
@@ -403,6 +484,44 @@ int dmpStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st, std::vector<cu
     d.needReady = false;
   }
   const bool star = starPlan(p);
+  if (d.sequenced) {
+    // deep halos over several split dims: exchange at the round start, no in-kernel waits,
+    // the round's last step signals its halo readers' completion
+    if (ph == 0)
+      if (int rc = seqRoundStart(d, d.epoch > 0 && !handshake, st))
+        return rc;
+    for (int q = 0; q < r; ++q) {
+      p.regionExt[q][0] = ext[q][0];
+      p.regionExt[q][1] = ext[q][1];
+    }
+    std::vector<int> written;
+    for (int k = 0; k < storedCount(g); ++k)
+      written.push_back(p.bind[static_cast<size_t>(storedField(g, k))]);
+    bool signalled = false;
+    if (ph == kl - 1 && nw) {
+      StarLaunch F{};
+      for (int di = 0; di < 2 * r; ++di)
+        if (d.nbr[di] >= 0) {
+          F.hs[di] = band[di];
+          F.nodata |= 1 << di;
+          F.peer_flag[di] = d.peerFlags[di];
+        }
+      F.fuse = 1;
+      F.cnt = d.cnt6;
+      F.cnt_accum = d.cntAccum;
+      F.put_epoch = d.epoch + 1;
+      p.fuse = F;
+      signalled = true;
+    }
+    if (int rc = planStep(p, st))
+      return rc;
+    for (int b : written)
+      d.dirty[static_cast<size_t>(b)] = 1;
+    if (signalled)
+      ++d.epoch;
+    d.phase = (ph + 1) % kl;
+    return HG_OK;
+  }
   // deep halos: the call's first put rewrites halos the neighbours read in the last step of
   // their previous call (e.g. wave's prev band), so it waits for the signal round that step
   // published (after a ready handshake everybody's earlier work is done anyway)
@@ -883,10 +1002,11 @@ int hg_dmp_create_ex(hg_plan *plan, const hg_decomp *dc, int64_t rank, const hg_
       int split = 0;
       for (int q = 0; q < dc->ndim; ++q)
         split += dc->grid[q] > 1 ? 1 : 0;
-      if (split > 1)
-        return setError(HG_EUNSUPPORTED, "deep halos need a grid that splits one dimension "
-                                         "(the extended region would read corner cells that "
-                                         "face exchanges do not carry)");
+      if (split > 1 && o.transport == HG_TRANSPORT_NCCL)
+        return setError(HG_EUNSUPPORTED, "deep halos over NCCL need a grid that splits one "
+                                         "dimension (the extended region reads corner cells "
+                                         "that face exchanges do not carry)");
+      d->sequenced = split > 1;
       for (int s = 0; s < dc->nswaps; ++s)
         for (int k = 0; k < dc->swaps[s].nexchanges; ++k) {
           const hg_exchange &e = dc->swaps[s].ex[k];

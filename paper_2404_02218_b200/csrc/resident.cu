@@ -28,6 +28,10 @@
 #include <cstdlib>
 #include <mutex>
 
+#ifndef HG_RES_KMAX
+#define HG_RES_KMAX 2
+#endif
+
 namespace hg {
 namespace {
 
@@ -233,7 +237,8 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
         return rowBase + (r < E ? r0 - E + r : r1 + r - E) * SP;
       };
       auto live = [&](int r) { return r < E ? hasAbove : hasBelow; };
-      constexpr int MW = 4; // up to 4 halo rows (K=2, R=1) polled concurrently: one round trip
+      // up to 2K halo rows (R = 1) polled concurrently: one round trip
+      constexpr int MW = 2 * HG_RES_KMAX > 4 ? 2 * HG_RES_KMAX : 4;
       for (int x = tid; x < nx; x += NTH) {
         if (2 * E <= MW) {
           W64 w[MW];
@@ -377,7 +382,7 @@ bool geometry(const ResLaunch &L, ResGeometry &g) {
     g.PL += 4;
   g.SP = (g.PL + W + 8 + 3) / 4 * 4;
   const size_t cap = 227 * 1024;
-  constexpr int kMax = 2; // steps per exchange: best of 1/2/4/6/8 (r1_sweeps.md)
+  constexpr int kMax = HG_RES_KMAX; // steps per exchange (r1_sweeps.md; round-2 A/B)
   for (int G = std::min(numSMs(), ny); G >= 1; --G) {
     const int minRows = ny / G, maxRows = (ny + G - 1) / G;
     int K = std::min(kMax, minRows / R); // steps per exchange

@@ -246,6 +246,12 @@ def test_stuck_peer_reports_instead_of_hanging():
     ("wave", 3, 8, "200x96x192", "1x1x2", 5, None, 2, "nccl"),
     ("heat", 3, 4, "192x256x128", "1x2x1", 6, "1,5", 2, "p2p"),     # y split
     ("heat", 3, 4, "400x64x96", "4x1x1", 7, "3,4", 2, "p2p"),
+    # several split dims: the sequenced (dim-ordered, corner-carrying) round exchange
+    ("heat", 3, 4, "192x128x256", "2x2x1", 6, "1,5", 2, "p2p"),
+    ("heat", 3, 4, "192x128x256", "1x2x2", 7, None, 2, "p2p"),
+    ("heat", 3, 2, "120x96x160", "2x1x2", 7, "4,3", 3, "p2p"),
+    ("wave", 3, 8, "160x96x96", "2x2x1", 5, "2,3", 2, "p2p"),
+    ("heat", 2, 2, "256x256", "2x2", 9, "4,5", 3, "p2p"),
 ])
 def test_ipc_dmp_deep_halo(kind, rank, order, extents, grid, T, calls, depth, transport):
     n = _ngpus()
@@ -266,7 +272,8 @@ def test_ipc_dmp_deep_halo(kind, rank, order, extents, grid, T, calls, depth, tr
 @pytest.mark.gpu
 @pytest.mark.parametrize("spec,grid,T,depth", [
     (("heat", 3, 48, 4), [2, 1, 1], 7, 2), (("wave", 3, 48, 8), [1, 1, 2], 5, 2),
-    (("heat", 3, 64, 2), [1, 4, 1], 7, 3),
+    (("heat", 3, 64, 2), [1, 4, 1], 7, 3), (("heat", 3, 64, 2), [2, 2, 1], 7, 3),
+    (("heat", 3, 48, 4), [1, 2, 2], 5, 2),
 ])
 def test_simulate_deep_halo(port, spec, grid, T, depth):
     # simulate with deep halos (one rank per GPU): gathered cores == the serial run
@@ -285,9 +292,9 @@ def test_simulate_deep_halo(port, spec, grid, T, depth):
 
 
 @pytest.mark.gpu
-def test_deep_halo_rejects_multi_dim_splits():
-    # the extended region of a deep round reads corner cells (the z band over the y halo) that
-    # face exchanges do not carry: grids splitting two dims are refused with a message
+def test_deep_halo_nccl_rejects_multi_dim_splits():
+    # over NCCL the deep round exchanges every face at once, so the corner cells a multi-dim
+    # split needs would be missing: refused with a message (P2P sequences the dims instead)
     import paper_2404_02218_b200 as hg
     prog = hg.build_kernel(hg.KernelSpec("heat", 3, 32, 4, "f32"))
     local, dc = prog.decompose([2, 2, 1], depth=2)
@@ -295,7 +302,7 @@ def test_deep_halo_rejects_multi_dim_splits():
     assert [h - l for l, h in zip(lo, hi)] == [24, 24, 36]  # deep halos 4, 4; unsplit 2
     plan = hg.Plan(local)
     try:
-        with pytest.raises(hg.HgError, match="splits one dimension"):
-            hg.Dmp(plan, dc, 0, depth=2)
+        with pytest.raises(hg.HgError, match="splits one"):
+            hg.Dmp(plan, dc, 0, transport="nccl", nccl_id=bytes(128), nranks=4, depth=2)
     finally:
         plan.close()
