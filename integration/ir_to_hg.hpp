@@ -14,6 +14,7 @@
 #define HG_INTEGRATION_IR_TO_HG_HPP
 
 #include "hg/hg.h"
+#include "halogen/exec/serial.hpp"
 #include "halogen/ir/ir.hpp"
 
 #include <cstring>
@@ -32,23 +33,10 @@ struct Converted {
   hg_decomp decomp{};
 };
 
+// the step function: the reference's own exec::stencilEntry (serial.hpp:22, serial.cpp:22-40:
+// the single func whose arguments are all fields); it only reads the module
 inline const halogen::ir::Operation *stencilEntry(const halogen::ir::Operation &module) {
-  using namespace halogen::ir;
-  const Operation *found = nullptr;
-  for (const auto &op : moduleBody(module).ops) {
-    if (op->name != "func.func" || op->regions.empty() || op->regions[0].args.empty())
-      continue;
-    bool allFields = true;
-    for (const Value &a : op->regions[0].args)
-      if (!a.type.is<FieldType>())
-        allFields = false;
-    if (!allFields)
-      continue;
-    if (found)
-      return nullptr;
-    found = op.get();
-  }
-  return found;
+  return halogen::exec::stencilEntry(const_cast<halogen::ir::Operation &>(module));
 }
 
 inline void boundsOf(const halogen::ir::Bounds &b, hg_bounds &out) {

@@ -783,6 +783,37 @@ int ncclStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st) {
   if (!xs.empty()) {
     NcclState &S = d.nc;
     const size_t es = static_cast<size_t>(p.lay[0].es);
+    const int r = p.prog.rank;
+    // my receive box of each exchange: the `at` of my exchange toward that neighbour
+    std::vector<Xjob> mine = xs;
+    for (size_t k = 0; k < xs.size(); ++k) {
+      const hg_swap &sw = d.dc.swaps[xs[k].swap];
+      for (int e = 0; e < sw.nexchanges; ++e) {
+        int dim, sign;
+        dirOf(sw.ex[e], r, &dim, &sign);
+        if (dirIndex(dim, sign) == xs[k].dir)
+          for (int q = 0; q < r; ++q)
+            mine[k].recv_at[q] = sw.ex[e].at[q];
+      }
+    }
+    // deep halos over several split dims: dim-ordered stages whose boxes span the halos of
+    // the dims before them (corners travel through two hops, as in seqRoundStart)
+    if (d.sequenced) {
+      int64_t W[HG_MAX_RANK] = {0, 0, 0};
+      for (const Xjob &x : xs)
+        W[x.dim] = std::max(W[x.dim], x.size[x.dim]);
+      for (size_t k = 0; k < xs.size(); ++k) {
+        xs[k].n = 1;
+        for (int e = 0; e < r; ++e) {
+          if (e < xs[k].dim && d.dc.grid[e] > 1) {
+            xs[k].send_at[e] -= W[e];
+            mine[k].recv_at[e] -= W[e];
+            xs[k].size[e] += 2 * W[e];
+          }
+          xs[k].n *= xs[k].size[e];
+        }
+      }
+    }
     if (S.sbuf.size() < xs.size()) {
       S.sbuf.resize(xs.size(), nullptr);
       S.rbuf.resize(xs.size(), nullptr);
@@ -802,51 +833,50 @@ int ncclStep(hg_dmp &d, int64_t t, int64_t steps, cudaStream_t st) {
         S.cap[k] = need;
       }
     }
-    for (size_t k = 0; k < xs.size(); ++k) {
-      const Xjob &x = xs[k];
-      if (int rc = launchPackUnpack(p.dptr[static_cast<size_t>(x.buffer)],
-                                    devLayout(p.lay[static_cast<size_t>(x.buffer)]), x.send_at,
-                                    x.size, S.sbuf[k], 0, st))
-        return rc;
-      ++p.launches;
-    }
+    // the comm stream starts once this step's inputs are final (the previous step is done)
     if (int rc = cudaCheck(cudaEventRecord(S.packed, st), "cudaEventRecord"))
       return rc;
     if (int rc = cudaCheck(cudaStreamWaitEvent(S.cs, S.packed, 0), "cudaStreamWaitEvent"))
       return rc;
     const ncclDataType_t dt = es == 4 ? ncclFloat32 : ncclFloat64;
-    if (int rc = ncclCheck(api.groupStart(), "ncclGroupStart"))
-      return rc;
-    for (size_t k = 0; k < xs.size(); ++k) {
-      const int peer = static_cast<int>(d.nbr[xs[k].dir]);
-      const size_t n = static_cast<size_t>(xs[k].n);
-      ncclResult_t r1 = api.send(S.sbuf[k], n, dt, peer, S.comm, S.cs);
-      ncclResult_t r2 = api.recv(S.rbuf[k], n, dt, peer, S.comm, S.cs);
-      if (r1 != ncclSuccess || r2 != ncclSuccess) {
-        api.groupEnd();
-        return ncclCheck(r1 != ncclSuccess ? r1 : r2, "ncclSend/ncclRecv");
+    // stages: every exchange at once, or (sequenced) one split dim after the other
+    for (int stage = 0; stage < (d.sequenced ? r : 1); ++stage) {
+      auto inStage = [&](const Xjob &x) { return !d.sequenced || x.dim == stage; };
+      for (size_t k = 0; k < xs.size(); ++k) {
+        if (!inStage(xs[k]))
+          continue;
+        if (int rc = launchPackUnpack(p.dptr[static_cast<size_t>(xs[k].buffer)],
+                                      devLayout(p.lay[static_cast<size_t>(xs[k].buffer)]),
+                                      xs[k].send_at, xs[k].size, S.sbuf[k], 0, S.cs))
+          return rc;
+        ++p.launches;
       }
-      d.bytes += xs[k].n * static_cast<int64_t>(es);
-    }
-    if (int rc = ncclCheck(api.groupEnd(), "ncclGroupEnd"))
-      return rc;
-    // receive into my halo: the box `at` of my exchange toward that neighbour
-    std::vector<Xjob> mine = xs;
-    for (size_t k = 0; k < xs.size(); ++k) {
-      const hg_swap &s = d.dc.swaps[xs[k].swap];
-      const int r = p.prog.rank;
-      for (int e = 0; e < s.nexchanges; ++e) {
-        int dim, sign;
-        dirOf(s.ex[e], r, &dim, &sign);
-        if (dirIndex(dim, sign) == xs[k].dir)
-          for (int q = 0; q < r; ++q)
-            mine[k].recv_at[q] = s.ex[e].at[q];
-      }
-      if (int rc = launchPackUnpack(p.dptr[static_cast<size_t>(xs[k].buffer)],
-                                    devLayout(p.lay[static_cast<size_t>(xs[k].buffer)]),
-                                    mine[k].recv_at, xs[k].size, S.rbuf[k], 1, S.cs))
+      if (int rc = ncclCheck(api.groupStart(), "ncclGroupStart"))
         return rc;
-      ++p.launches;
+      for (size_t k = 0; k < xs.size(); ++k) {
+        if (!inStage(xs[k]))
+          continue;
+        const int peer = static_cast<int>(d.nbr[xs[k].dir]);
+        const size_t n = static_cast<size_t>(xs[k].n);
+        ncclResult_t r1 = api.send(S.sbuf[k], n, dt, peer, S.comm, S.cs);
+        ncclResult_t r2 = api.recv(S.rbuf[k], n, dt, peer, S.comm, S.cs);
+        if (r1 != ncclSuccess || r2 != ncclSuccess) {
+          api.groupEnd();
+          return ncclCheck(r1 != ncclSuccess ? r1 : r2, "ncclSend/ncclRecv");
+        }
+        d.bytes += xs[k].n * static_cast<int64_t>(es);
+      }
+      if (int rc = ncclCheck(api.groupEnd(), "ncclGroupEnd"))
+        return rc;
+      for (size_t k = 0; k < xs.size(); ++k) {
+        if (!inStage(xs[k]))
+          continue;
+        if (int rc = launchPackUnpack(p.dptr[static_cast<size_t>(xs[k].buffer)],
+                                      devLayout(p.lay[static_cast<size_t>(xs[k].buffer)]),
+                                      mine[k].recv_at, xs[k].size, S.rbuf[k], 1, S.cs))
+          return rc;
+        ++p.launches;
+      }
     }
     if (int rc = cudaCheck(cudaEventRecord(S.halo, S.cs), "cudaEventRecord"))
       return rc;
@@ -1002,11 +1032,7 @@ int hg_dmp_create_ex(hg_plan *plan, const hg_decomp *dc, int64_t rank, const hg_
       int split = 0;
       for (int q = 0; q < dc->ndim; ++q)
         split += dc->grid[q] > 1 ? 1 : 0;
-      if (split > 1 && o.transport == HG_TRANSPORT_NCCL)
-        return setError(HG_EUNSUPPORTED, "deep halos over NCCL need a grid that splits one "
-                                         "dimension (the extended region reads corner cells "
-                                         "that face exchanges do not carry)");
-      d->sequenced = split > 1;
+      d->sequenced = split > 1; // dim-ordered round exchange (P2P: seqRoundStart; NCCL: stages)
       for (int s = 0; s < dc->nswaps; ++s)
         for (int k = 0; k < dc->swaps[s].nexchanges; ++k) {
           const hg_exchange &e = dc->swaps[s].ex[k];

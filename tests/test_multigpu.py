@@ -252,6 +252,8 @@ def test_stuck_peer_reports_instead_of_hanging():
     ("heat", 3, 2, "120x96x160", "2x1x2", 7, "4,3", 3, "p2p"),
     ("wave", 3, 8, "160x96x96", "2x2x1", 5, "2,3", 2, "p2p"),
     ("heat", 2, 2, "256x256", "2x2", 9, "4,5", 3, "p2p"),
+    ("heat", 3, 4, "192x128x256", "2x2x1", 6, "1,5", 2, "nccl"),   # NCCL, dim-ordered stages
+    ("wave", 3, 8, "160x96x96", "1x2x2", 5, None, 2, "nccl"),
 ])
 def test_ipc_dmp_deep_halo(kind, rank, order, extents, grid, T, calls, depth, transport):
     n = _ngpus()
@@ -289,20 +291,3 @@ def test_simulate_deep_halo(port, spec, grid, T, depth):
     perm = port.run(prog, arrays, T)
     for b, p in zip(out, perm):
         assert np.array_equal(b.data.view(np.uint32), arrays[p].view(np.uint32))
-
-
-@pytest.mark.gpu
-def test_deep_halo_nccl_rejects_multi_dim_splits():
-    # over NCCL the deep round exchanges every face at once, so the corner cells a multi-dim
-    # split needs would be missing: refused with a message (P2P sequences the dims instead)
-    import paper_2404_02218_b200 as hg
-    prog = hg.build_kernel(hg.KernelSpec("heat", 3, 32, 4, "f32"))
-    local, dc = prog.decompose([2, 2, 1], depth=2)
-    lo, hi = local.field_bounds(0)
-    assert [h - l for l, h in zip(lo, hi)] == [24, 24, 36]  # deep halos 4, 4; unsplit 2
-    plan = hg.Plan(local)
-    try:
-        with pytest.raises(hg.HgError, match="splits one"):
-            hg.Dmp(plan, dc, 0, transport="nccl", nccl_id=bytes(128), nranks=4, depth=2)
-    finally:
-        plan.close()
