@@ -225,13 +225,14 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
       const W64 *above = xw + (size_t(par) * G + (c - 1)) * 2 * slot + slot;
       const W64 *below = xw + (size_t(par) * G + (c + 1)) * 2 * slot;
       const bool hasAbove = c > 0, hasBelow = c + 1 < G;
+      // (no memory clobber: the tag carries validity, the tile store depends on the value)
       auto ldw = [](const W64 *q) {
         W64 w;
-        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(q) : "memory");
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(q));
         return w;
       };
-      auto srcOf = [&](int r, int x) {
-        return r < E ? above + size_t(r) * nx + x : below + size_t(r - E) * nx + x;
+      auto srcOf = [&](int r, int x) { // 32-bit row offsets: the slots are < 2^31 words
+        return r < E ? above + (r * nx + x) : below + ((r - E) * nx + x);
       };
       auto dstOf = [&](int r) { // tile offset of halo row r at store column 0
         return rowBase + (r < E ? r0 - E + r : r1 + r - E) * SP;
