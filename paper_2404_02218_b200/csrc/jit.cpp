@@ -221,7 +221,7 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   s << "typedef " << T << " T;\n";
   s << "struct P_t { TMap tm[" << O << "]; T *out[" << p.nresults << "];\n"
     << "  long long plane, pitch, col0; int zs, ys, xs, nz, ny, nx, tiles_x, tiles_y, chunk, "
-       "nchunks; };\n";
+       "nchunks, units; };\n";
   s << "struct __align__(16) V4 { T v[4]; };\n";
   s << "__device__ __forceinline__ V4 ld4(const T *q) { V4 r; ";
   if (es == 4)
@@ -247,29 +247,35 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
        "  T *stages = (T *)(sm + ((128u - (sma(sm) & 127u)) & 127u));\n"
        "  u64 *full = (u64 *)(stages + (size_t)NS * O * SS);\n"
        "  u64 *empty = full + NS;\n"
-       "  int u = blockIdx.x;\n"
-       "  const int txi = u % P.tiles_x; u /= P.tiles_x;\n"
-       "  const int tyi = u % P.tiles_y; const int chunk = u / P.tiles_y;\n"
-       "  const int xb = txi * TX, yb = tyi * TY, zb = chunk * P.chunk;\n"
-       "  const int n = min(P.chunk, P.nz - zb);\n"
        "  const int tid = threadIdx.x;\n"
        "  if (tid == 0) { for (int s = 0; s < NS; ++s) { mb_init(&full[s], 1); "
        "mb_init(&empty[s], NCONS); }\n"
        "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\"); }\n"
        "  __syncthreads();\n"
-       "  if (n <= 0) return;\n";
-  // producer
+       "  int xb, yb, zb, n;\n"
+       "  auto unit = [&](int u) {\n"
+       "    const int txi = u % P.tiles_x; u /= P.tiles_x;\n"
+       "    const int tyi = u % P.tiles_y; const int chunk = u / P.tiles_y;\n"
+       "    xb = txi * TX; yb = tyi * TY; zb = chunk * P.chunk;\n"
+       "    n = min(P.chunk, P.nz - zb);\n"
+       "  };\n";
+  // producer: one elected thread streams every unit's planes through one ring, so the next
+  // unit's first planes are in flight while the consumers finish the current one
   s << "  if (tid >= NCONS) {\n"
        "    if (tid == NCONS) {\n"
-       "      const int cx = (int)P.col0 + P.xs + xb - 4;\n"
-    << "      const int cy = " << (r == 3 ? "P.ys + yb - RY" : "0") << ";\n"
-    << "      const int z0 = P.zs + zb - RZ;\n"
-       "      for (int i = 0; i < n + 2 * RZ; ++i) {\n"
-       "        const int s = i % NS;\n"
-       "        if (i >= NS) mb_wait(&empty[s], (u32)((i / NS - 1) & 1));\n"
-       "        mb_expect(&full[s], (u32)(O * (TY + 2 * RY) * CW * sizeof(T)));\n"
-       "        for (int o = 0; o < O; ++o)\n"
-       "          tma3(stages + ((size_t)s * O + o) * SS, &P.tm[o], &full[s], cx, cy, z0 + i);\n"
+       "      int s = 0, ph = 0, g = 0;\n"
+       "      for (int u = blockIdx.x; u < P.units; u += gridDim.x) {\n"
+       "        unit(u);\n"
+       "        const int cx = (int)P.col0 + P.xs + xb - 4;\n"
+    << "        const int cy = " << (r == 3 ? "P.ys + yb - RY" : "0") << ";\n"
+    << "        const int z0 = P.zs + zb - RZ;\n"
+       "        for (int i = 0; i < n + 2 * RZ; ++i, ++g) {\n"
+       "          if (g >= NS) mb_wait(&empty[s], (u32)(ph ^ 1));\n"
+       "          mb_expect(&full[s], (u32)(O * (TY + 2 * RY) * CW * sizeof(T)));\n"
+       "          for (int o = 0; o < O; ++o)\n"
+       "            tma3(stages + ((size_t)s * O + o) * SS, &P.tm[o], &full[s], cx, cy, z0 + i);\n"
+       "          if (++s == NS) { s = 0; ph ^= 1; }\n"
+       "        }\n"
        "      }\n"
        "    }\n"
        "    return;\n"
@@ -277,15 +283,19 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   // consumers
   s << "  const int tx = tid % TXT, ty = tid / TXT, x0 = tx * 4;\n"
        "  const int rowOwn = (ty + RY) * CW + 4 + x0;\n"
+       "  int sOld = 0;          // stage of plane m (oldest in the window)\n"
+       "  int sNew = 0, phNew = 0;\n"
+       "  for (int u = blockIdx.x; u < P.units; u += gridDim.x) {\n"
+       "  unit(u);\n"
     << "  const bool yok = " << (r == 3 ? "yb + ty < P.ny" : "true") << ";\n"
     << "  const int xrem = P.nx - (xb + x0);\n"
-       "  const long long obase = (long long)(P.zs + zb) * P.plane + "
+       "  long long ebase = (long long)(P.zs + zb) * P.plane + "
     << (r == 3 ? "(long long)(P.ys + yb + ty) * P.pitch + " : "")
-    << "P.col0 + P.xs + xb + x0;\n"
-       "  for (int i = 0; i < 2 * RZ; ++i) mb_wait(&full[i % NS], (u32)((i / NS) & 1));\n"
-       "  int sOld = 0;          // stage of plane m (oldest in the window)\n"
-       "  long long ebase = obase; // output element of plane m\n"
-       "  int sNew = (2 * RZ) % NS, phNew = ((2 * RZ) / NS) & 1;\n"
+    << "P.col0 + P.xs + xb + x0; // output element of plane m\n"
+       "  for (int i = 0; i < 2 * RZ; ++i) {\n"
+       "    mb_wait(&full[sNew], (u32)phNew);\n"
+       "    if (++sNew == NS) { sNew = 0; phNew ^= 1; }\n"
+       "  }\n"
        "  for (int m = 0; m < n; ++m) {\n"
        "    mb_wait(&full[sNew], (u32)phNew);\n"
        "    if (++sNew == NS) { sNew = 0; phNew ^= 1; }\n";
@@ -358,7 +368,13 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   s << "    ebase += P.plane;\n"
        "    mb_arrive(&empty[sOld]);\n"
        "    if (++sOld == NS) sOld = 0;\n";
+  // the unit's last 2RZ planes were read by its last outputs, stored above: release them
   s << "  }\n"
+       "  for (int i = 0; i < 2 * RZ; ++i) {\n"
+       "    mb_arrive(&empty[sOld]);\n"
+       "    if (++sOld == NS) sOld = 0;\n"
+       "  }\n"
+       "  }\n"
        "}\n";
   K.source = s.str();
   return HG_OK;
@@ -403,11 +419,15 @@ int jitLoad(JitKernel &K, int device) {
     return setError(HG_ECUDA, std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e));
   K.lib = lib;
   K.kernel = k;
-  (void)device;
   e = cudaFuncSetAttribute(reinterpret_cast<const void *>(k),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(K.smem));
   if (e != cudaSuccess)
     return setError(HG_ECUDA, std::string("cudaFuncSetAttribute(jit): ") + cudaGetErrorString(e));
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&K.resident, reinterpret_cast<const void *>(k),
+                                                    K.nthreads, K.smem);
+  if (e != cudaSuccess || K.resident < 1)
+    return setError(HG_ECUDA, "fused apply: no CTA fits an SM");
+  cudaDeviceGetAttribute(&K.sms, cudaDevAttrMultiProcessorCount, device);
   return HG_OK;
 }
 
@@ -443,7 +463,8 @@ int jitTensorMap(const JitKernel &K, int dtype, int rank, const Layout &lay, voi
 }
 
 int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
-              const CUtensorMap *const *tms, void *const *outs, int chunks, cudaStream_t st) {
+              const CUtensorMap *const *tms, void *const *outs, int chunks, bool persist,
+              cudaStream_t st) {
   // must mirror struct P_t of the generated source
   struct alignas(64) TMap {
     unsigned long long w[16];
@@ -453,7 +474,7 @@ int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
   };
   const int O = p.noperands, KR = p.nresults, r = p.rank;
   // pack the parameter block exactly like P_t: TMap tm[O]; T *out[KR]; long long plane,
-  // pitch, col0; int zs, ys, xs, nz, ny, nx, tiles_x, tiles_y, chunk, nchunks;
+  // pitch, col0; int zs, ys, xs, nz, ny, nx, tiles_x, tiles_y, chunk, nchunks, units;
   alignas(64) unsigned char buf[8 * 128 + 8 * 8 + 3 * 8 + 10 * 4 + 64];
   std::memset(buf, 0, sizeof buf);
   size_t at = 0;
@@ -491,12 +512,16 @@ int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
   int nch = chunks > 0 ? chunks : std::max(1, (nz + zc / 2) / zc);
   int chunk = (nz + nch - 1) / nch;
   nch = (nz + chunk - 1) / chunk;
-  int iv[10] = {zs, ys, xs, nz, ny, nx, tiles_x, tiles_y, chunk, nch};
+  const int units = tiles_x * tiles_y * nch;
+  int iv[11] = {zs, ys, xs, nz, ny, nx, tiles_x, tiles_y, chunk, nch, units};
   std::memcpy(buf + at, iv, sizeof iv);
   at += sizeof iv;
   (void)Params{};
   void *args[] = {buf};
-  const unsigned blocks = unsigned(tiles_x) * tiles_y * nch;
+  // persistent: one wave of resident CTAs, each walking units blockIdx.x + k * gridDim.x with
+  // its TMA ring running across unit boundaries; otherwise one CTA per unit
+  const unsigned blocks =
+      persist ? unsigned(std::min(units, K.resident * K.sms)) : unsigned(units);
   cudaError_t e = cudaLaunchKernel(reinterpret_cast<const void *>(K.kernel), dim3(blocks),
                                    dim3(K.nthreads), args, K.smem, st);
   if (e != cudaSuccess)

@@ -19,6 +19,7 @@ struct JitKernel {
   cudaKernel_t kernel = nullptr;
   int rz = 0, ry = 0, txt = 16, tyt = 16, tx = 64, ty = 16, ns = 0, ncons = 0, nthreads = 0;
   int deep = 0; // TMA ring depth beyond the 2RZ+1 window (0 = auto; chunk sizing follows it)
+  int resident = 1, sms = 148; // CTAs per SM at this block/smem size, SMs of the device
   size_t smem = 0;
 };
 
@@ -31,7 +32,8 @@ int jitLoad(JitKernel &K, int device);                    // current device
 int jitTensorMap(const JitKernel &K, int dtype, int rank, const Layout &lay, void *base,
                  CUtensorMap *out);
 int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
-              const CUtensorMap *const *tms, void *const *outs, int chunks, cudaStream_t st);
+              const CUtensorMap *const *tms, void *const *outs, int chunks, bool persist,
+              cudaStream_t st);
 
 } // namespace hg
 

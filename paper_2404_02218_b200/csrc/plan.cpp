@@ -289,7 +289,7 @@ int multiStep(hg_plan &p, cudaStream_t st) {
         outs[k] = f >= 0 ? p.dptr[static_cast<size_t>(p.bind[static_cast<size_t>(f)])]
                          : p.tmpPtr[static_cast<size_t>(A.result_temp[k])];
       }
-      int rc = jitLaunch(*M.jit, M.sub, p.lay[0], tms, outs, 0, st);
+      int rc = jitLaunch(*M.jit, M.sub, p.lay[0], tms, outs, 0, p.knobs.jitPersist, st);
       if (rc)
         return rc;
       ++p.launches;
@@ -474,7 +474,7 @@ int planStep(hg_plan &p, cudaStream_t st) {
       tms[o] = &p.tmApply[static_cast<size_t>(p.bind[static_cast<size_t>(g.operand_field[o])])];
     for (int k = 0; k < g.nresults; ++k)
       outs[k] = p.dptr[static_cast<size_t>(p.bind[static_cast<size_t>(g.store_field[k])])];
-    int st2 = jitLaunch(*p.jit, g, p.lay[0], tms, outs, p.chunks, st);
+    int st2 = jitLaunch(*p.jit, g, p.lay[0], tms, outs, p.chunks, p.knobs.jitPersist, st);
     if (st2)
       return st2;
   } else {
