@@ -55,6 +55,8 @@ struct Knobs {
   int starGeo = -1;           // HG_STAR_GEO=n: force the star tile geometry
   int jitDepth = 0;           // HG_JIT_DEPTH=n: TMA ring depth of the fused-apply family
   bool jitPersist = true;     // HG_JIT_PERSIST=0: fused-apply family one CTA per unit
+  bool jitPack = false;       // HG_JIT_PACK=1: fused-apply family f32 adds as FADD2 (PW set:
+                              // neutral, profiles/r2_ab.md)
   int pitchPad = 0;           // HG_PITCH_PAD=n: n extra 128-byte lines per row (layout A/B)
   bool guards = false;        // HG_DEBUG_GUARDS=1: canary bands around every device buffer of
                               // the plan (hg_plan_check_guards finds out-of-bounds writes)

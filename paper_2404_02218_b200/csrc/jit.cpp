@@ -89,6 +89,25 @@ __device__ __forceinline__ void mb_wait(u64 *b, u32 ph) {
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(d) : "r"(sma(b)), "r"(ph) : "memory");
   } while (!d);
 }
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(f2 v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ void tma3(void *dst, const TMap *m, u64 *b, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
                "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(sma(dst)), "l"((u64)m), "r"(c0), "r"(c1),
@@ -167,6 +186,8 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   }
   K.rz = rz;
   K.ry = ry;
+  if (p.dtype != HG_F32)
+    K.pack = false;
   K.txt = r == 3 ? 16 : 32;
   K.tyt = r == 3 ? 16 : 1;
   K.tx = K.txt * 4;
@@ -316,40 +337,88 @@ int jitBuildSource(const hg_program &p, JitKernel &K) {
   // the DAG, 4 points
   for (int k = 0; k < p.nresults; ++k)
     s << "    V4 res" << k << ";\n";
-  for (int j = 0; j < 4; ++j) {
-    s << "    {\n";
-    for (int i = 0; i < p.nops; ++i) {
-      const hg_op &o = p.ops[i];
-      s << "      const T v" << i << " = ";
-      switch (o.code) {
-      case HG_OP_ACCESS: {
-        const int dz = static_cast<int>(o.off[0]), dy = r == 3 ? static_cast<int>(o.off[1]) : 0,
-                  dx = static_cast<int>(o.off[r - 1]);
-        const int idx = 4 + j + dx;
-        s << "w" << o.operand << "_" << (dz + rz) << "_" << (dy + 8) << "c" << idx / 4 << ".v["
-          << idx % 4 << "]";
-        break;
-      }
-      case HG_OP_CONST:
-        s << constLiteral(o.bits, p.dtype);
-        break;
-      case HG_OP_ADD:
-        s << add << "(v" << o.a << ", v" << o.b << ")";
-        break;
-      case HG_OP_SUB:
-        s << sub << "(v" << o.a << ", v" << o.b << ")";
-        break;
-      case HG_OP_MUL:
-        s << mul << "(v" << o.a << ", v" << o.b << ")";
-        break;
-      default:
-        s << div << "(v" << o.a << ", v" << o.b << ")";
-      }
-      s << ";\n";
+  auto access = [&](const hg_op &o, int j) {
+    const int dz = static_cast<int>(o.off[0]), dy = r == 3 ? static_cast<int>(o.off[1]) : 0,
+              dx = static_cast<int>(o.off[r - 1]);
+    const int idx = 4 + j + dx;
+    return "w" + std::to_string(o.operand) + "_" + std::to_string(dz + rz) + "_" +
+           std::to_string(dy + 8) + "c" + std::to_string(idx / 4) + ".v[" +
+           std::to_string(idx % 4) + "]";
+  };
+  auto binop = [&](const hg_op &o) {
+    switch (o.code) {
+    case HG_OP_ADD:
+      return add;
+    case HG_OP_SUB:
+      return sub;
+    case HG_OP_MUL:
+      return mul;
+    default:
+      return div;
     }
-    for (int k = 0; k < p.nresults; ++k)
-      s << "      res" << k << ".v[" << j << "] = v" << p.result_op[k] << ";\n";
-    s << "    }\n";
+  };
+  if (K.pack) {
+    // f32: points (j, j+1) as one f32x2 lane pair for every add/sub (FADD2); products and
+    // quotients stay scalar, so ptxas has no packed multiply to contract (bit-exact: each lane
+    // is the scalar RN op).  An add reading an x access at an odd offset (its pair straddles
+    // two 16-byte windows' register halves) stays scalar too.
+    auto oddX = [&](int v) {
+      const hg_op &o = p.ops[v];
+      return o.code == HG_OP_ACCESS && (o.off[r - 1] % 2) != 0;
+    };
+    for (int jp = 0; jp < 4; jp += 2) {
+      s << "    {\n";
+      for (int i = 0; i < p.nops; ++i) {
+        const hg_op &o = p.ops[i];
+        const std::string a0 = "v" + std::to_string(o.a) + "_0", a1 = "v" + std::to_string(o.a) + "_1";
+        const std::string b0 = "v" + std::to_string(o.b) + "_0", b1 = "v" + std::to_string(o.b) + "_1";
+        const std::string v0 = "v" + std::to_string(i) + "_0", v1 = "v" + std::to_string(i) + "_1";
+        switch (o.code) {
+        case HG_OP_ACCESS:
+          s << "      const T " << v0 << " = " << access(o, jp) << ", " << v1 << " = "
+            << access(o, jp + 1) << ";\n";
+          break;
+        case HG_OP_CONST:
+          s << "      const T " << v0 << " = " << constLiteral(o.bits, p.dtype) << ", " << v1
+            << " = " << v0 << ";\n";
+          break;
+        case HG_OP_ADD:
+        case HG_OP_SUB:
+          if (!oddX(o.a) && !oddX(o.b)) {
+            s << "      T " << v0 << ", " << v1 << "; upk2("
+              << (o.code == HG_OP_ADD ? "add2" : "sub2") << "(pk2(" << a0 << ", " << a1
+              << "), pk2(" << b0 << ", " << b1 << ")), " << v0 << ", " << v1 << ");\n";
+            break;
+          }
+          [[fallthrough]];
+        default:
+          s << "      const T " << v0 << " = " << binop(o) << "(" << a0 << ", " << b0 << "), "
+            << v1 << " = " << binop(o) << "(" << a1 << ", " << b1 << ");\n";
+        }
+      }
+      for (int k = 0; k < p.nresults; ++k)
+        s << "      res" << k << ".v[" << jp << "] = v" << p.result_op[k] << "_0; res" << k
+          << ".v[" << jp + 1 << "] = v" << p.result_op[k] << "_1;\n";
+      s << "    }\n";
+    }
+  } else {
+    for (int j = 0; j < 4; ++j) {
+      s << "    {\n";
+      for (int i = 0; i < p.nops; ++i) {
+        const hg_op &o = p.ops[i];
+        s << "      const T v" << i << " = ";
+        if (o.code == HG_OP_ACCESS)
+          s << access(o, j);
+        else if (o.code == HG_OP_CONST)
+          s << constLiteral(o.bits, p.dtype);
+        else
+          s << binop(o) << "(v" << o.a << ", v" << o.b << ")";
+        s << ";\n";
+      }
+      for (int k = 0; k < p.nresults; ++k)
+        s << "      res" << k << ".v[" << j << "] = v" << p.result_op[k] << ";\n";
+      s << "    }\n";
+    }
   }
   s << "    if (yok) {\n"
        "      const long long e = ebase;\n";

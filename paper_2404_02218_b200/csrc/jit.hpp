@@ -20,6 +20,7 @@ struct JitKernel {
   int rz = 0, ry = 0, txt = 16, tyt = 16, tx = 64, ty = 16, ns = 0, ncons = 0, nthreads = 0;
   int deep = 0; // TMA ring depth beyond the 2RZ+1 window (0 = auto; chunk sizing follows it)
   int resident = 1, sms = 148; // CTAs per SM at this block/smem size, SMs of the device
+  bool pack = false; // f32: adds/subs of point pairs as f32x2 (FADD2); products scalar
   size_t smem = 0;
 };
 

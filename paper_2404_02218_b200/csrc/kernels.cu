@@ -109,11 +109,14 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
   static constexpr int TXT = 32, TYT = 1, PTS = 4;
 };
 
-// f32 star arithmetic on packed f32x2 pairs: bit-exact, but measured 4-8% slower than the
-// scalar form (pair-forming moves, fences, weight registers; profiles/r1_sweeps.md), so the
-// product builds the scalar form; HG_PACK=1 builds the packed one for A/B
+// f32 star arithmetic on f32x2 pairs of neighbouring points (bit-exact: each lane is the
+// scalar RN op).  HG_PACK=2 (product): sums and accumulations as FADD2, every product a scalar
+// FMUL, so ptxas has no mul.f32x2 -> add.f32x2 pair to contract into FFMA2 and no fence is
+// needed; 112 -> ~93 instructions per 4-point plane, +3% burst and +7% sustained (power-capped)
+// on heat 1024^3 (profiles/r2_ab.md).  HG_PACK=1: products packed too, every product fenced
+// (round 1: 4-8% slower, profiles/r1_sweeps.md).  HG_PACK=0: scalar.
 #ifndef HG_PACK
-#define HG_PACK 0
+#define HG_PACK 2
 #endif
 #ifndef HG_MINB_G2
 #define HG_MINB_G2 3
@@ -132,7 +135,9 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
 #ifndef HG_L2HINT
 #define HG_L2HINT 1
 #endif
-template <typename T> constexpr bool kPackF32 = HG_PACK && std::is_same<T, float>::value;
+template <typename T> constexpr bool kPackF32 = HG_PACK == 1 && std::is_same<T, float>::value;
+// HG_PACK=2: x taps at odd offsets (pairs straddling two registers' halves) add scalar
+template <typename T> constexpr bool kPackAdd = HG_PACK == 2 && std::is_same<T, float>::value;
 
 template <typename T> struct StarParams {
   int64_t plane;   // elements between consecutive dim-0 planes
@@ -540,6 +545,52 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
                    pfence(mul2(acc, P.pscale), z0));
         else
           r = add2(c, pfence(mul2(acc, P.pscale), z0));
+        upk2(r, o[j], o[j + 1]);
+      }
+    } else if constexpr (kPackAdd<T> && PTS == 4) {
+      // points (j, j+1): the scalar branch's op sequence, sums and accumulations as f32x2
+      auto win = [&](int i) -> T { // window [L | centre | Rr]
+        return i < 4 ? L.v[i & 3] : (i < 8 ? q[cz][i & 3] : Rr.v[i & 3]);
+      };
+      auto mulp = [&](f2 v, T w) -> f2 {
+        T a, b;
+        upk2(v, a, b);
+        return pk2(mul_(a, w), mul_(b, w));
+      };
+#pragma unroll
+      for (int j = 0; j < 4; j += 2) {
+        const T c0 = q[cz][j], c1 = q[cz][j + 1];
+        f2 acc = pk2(mul_(c0, P.w0), mul_(c1, P.w0));
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int k = Taps<NT>::k(t);
+          const int zp = (U + R + k) % Q, zm = (U + R - k + Q) % Q;
+          acc = add2(acc, mulp(add2(pk2(q[zp][j], q[zp][j + 1]), pk2(q[zm][j], q[zm][j + 1])),
+                               P.wz[t]));
+        }
+        if constexpr (RANK == 3) {
+#pragma unroll
+          for (int t = 0; t < NT; ++t)
+            acc = add2(acc, mulp(add2(pk2(yp[t][0].v[j], yp[t][0].v[j + 1]),
+                                      pk2(ym[t][0].v[j], ym[t][0].v[j + 1])),
+                                 P.wy[t]));
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int k = Taps<NT>::k(t);
+          f2 sum;
+          if (k % 2 == 0) // (4+j+k, 5+j+k) sits inside one 16-byte window: an aligned pair
+            sum = add2(pk2(win(4 + j + k), win(5 + j + k)), pk2(win(4 + j - k), win(5 + j - k)));
+          else
+            sum = pk2(add_(win(4 + j + k), win(4 + j - k)), add_(win(5 + j + k), win(5 + j - k)));
+          acc = add2(acc, mulp(sum, P.wx[t]));
+        }
+        f2 r;
+        if constexpr (C::WAVE)
+          r = add2(sub2(pk2(mul_(c0, P.two), mul_(c1, P.two)), pk2(pv[0].v[j], pv[0].v[j + 1])),
+                   mulp(acc, P.scale));
+        else
+          r = add2(pk2(c0, c1), mulp(acc, P.scale));
         upk2(r, o[j], o[j + 1]);
       }
     } else {

@@ -21,11 +21,12 @@ int cudaCheck(cudaError_t e, const char *what) {
 namespace {
 
 // Generated kernels are cached per (source, device): NVRTC runs once per distinct program.
-std::shared_ptr<JitKernel> jitCached(const hg_program &g, int device, int depth) {
+std::shared_ptr<JitKernel> jitCached(const hg_program &g, int device, const Knobs &kn) {
   static std::mutex mu;
   static std::map<std::pair<std::string, int>, std::shared_ptr<JitKernel>> cache;
   auto k = std::make_shared<JitKernel>();
-  k->deep = depth;
+  k->deep = kn.jitDepth;
+  k->pack = kn.jitPack;
   if (jitBuildSource(g, *k) != HG_OK)
     return nullptr;
   std::lock_guard<std::mutex> lk(mu);
@@ -193,7 +194,7 @@ bool compileMultiJit(hg_plan &p, int device, int &st) {
     Analysis none;
     if (!jitEligible(S, none, nullptr))
       return false;
-    M.jit = jitCached(S, device, p.knobs.jitDepth);
+    M.jit = jitCached(S, device, p.knobs);
     if (!M.jit)
       return false;
   }
@@ -644,7 +645,7 @@ int hg_plan_create(const hg_program *prog, int device, hg_plan **out) {
     // rims cover the accesses, else the slot-interpreting generic kernel
     std::string why;
     if (!p->knobs.noApplyJit && jitEligible(g, p->an, &why)) {
-      auto k = jitCached(g, device, p->knobs.jitDepth);
+      auto k = jitCached(g, device, p->knobs);
       if (k) {
         p->jit = k;
         p->an.family = Family::Apply;

@@ -452,6 +452,7 @@ Knobs readKnobs() {
   k.starGeo = num("HG_STAR_GEO", -1);
   k.jitDepth = std::max(0, num("HG_JIT_DEPTH", 0));
   k.jitPersist = num("HG_JIT_PERSIST", 1) != 0;
+  k.jitPack = num("HG_JIT_PACK", 0) != 0;
   k.guards = on("HG_DEBUG_GUARDS");
   k.pitchPad = std::max(0, num("HG_PITCH_PAD", 0));
   return k;
