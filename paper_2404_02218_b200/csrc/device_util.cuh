@@ -30,6 +30,15 @@ __device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a,
 // add.rn.f32x2 into FFMA2 even under -fmad=false (profiles/r1_sweeps.md); pfence() makes a
 // product opaque (OR of a run-time zero into its low word, one ALU op) so every product is
 // rounded before its add, exactly as the reference's -ffp-contract=off code does.
+// f32 stencil arithmetic (star and resident kernels) on f32x2 pairs of neighbouring points
+// (bit-exact: each lane is the scalar RN op).  HG_PACK=2 (product): sums and accumulations as FADD2, every product a scalar
+// FMUL, so ptxas has no mul.f32x2 -> add.f32x2 pair to contract into FFMA2 and no fence is
+// needed; 112 -> ~93 instructions per 4-point plane, +3% burst and +7% sustained (power-capped)
+// on heat 1024^3 (profiles/r2_ab.md).  HG_PACK=1: products packed too, every product fenced
+// (round 1: 4-8% slower, profiles/r1_sweeps.md).  HG_PACK=0: scalar.
+#ifndef HG_PACK
+#define HG_PACK 2
+#endif
 using f2 = unsigned long long;
 __device__ __forceinline__ f2 pk2(float lo, float hi) {
   f2 r;

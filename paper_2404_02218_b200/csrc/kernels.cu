@@ -109,15 +109,6 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
   static constexpr int TXT = 32, TYT = 1, PTS = 4;
 };
 
-// f32 star arithmetic on f32x2 pairs of neighbouring points (bit-exact: each lane is the
-// scalar RN op).  HG_PACK=2 (product): sums and accumulations as FADD2, every product a scalar
-// FMUL, so ptxas has no mul.f32x2 -> add.f32x2 pair to contract into FFMA2 and no fence is
-// needed; 112 -> ~93 instructions per 4-point plane, +3% burst and +7% sustained (power-capped)
-// on heat 1024^3 (profiles/r2_ab.md).  HG_PACK=1: products packed too, every product fenced
-// (round 1: 4-8% slower, profiles/r1_sweeps.md).  HG_PACK=0: scalar.
-#ifndef HG_PACK
-#define HG_PACK 2
-#endif
 #ifndef HG_MINB_G2
 #define HG_MINB_G2 3
 #endif

@@ -143,6 +143,41 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
           const V4<T> L = ld4(row + h * SP - 4), Rr = ld4(row + h * SP + 4);
           const V4<T> &Cc = cen[R + h];
           V4<T> o;
+          if constexpr (HG_PACK == 2 && std::is_same<T, float>::value) {
+            // points (j, j+1) as an f32x2 pair for the sums and accumulations, products
+            // scalar (the star kernel's packed-add form, kernels.cu); odd x taps add scalar
+            auto win = [&](int i) -> T { return i < 4 ? L.v[i & 3] : (i < 8 ? Cc.v[i & 3] : Rr.v[i & 3]); };
+            auto mulp = [&](f2 v, T w) -> f2 {
+              T a, b;
+              upk2(v, a, b);
+              return pk2(mul_(a, w), mul_(b, w));
+            };
+#pragma unroll
+            for (int j = 0; j < 4; j += 2) {
+              const T c0 = Cc.v[j], c1 = Cc.v[j + 1];
+              f2 acc = pk2(mul_(c0, P.w0), mul_(c1, P.w0));
+#pragma unroll
+              for (int t = 0; t < NT; ++t) {
+                const int k = Taps<NT>::k(t);
+                acc = add2(acc, mulp(add2(pk2(cen[R + h + k].v[j], cen[R + h + k].v[j + 1]),
+                                          pk2(cen[R + h - k].v[j], cen[R + h - k].v[j + 1])),
+                                     P.wz[t]));
+              }
+#pragma unroll
+              for (int t = 0; t < NT; ++t) {
+                const int k = Taps<NT>::k(t);
+                f2 sum;
+                if (k % 2 == 0)
+                  sum = add2(pk2(win(4 + j + k), win(5 + j + k)),
+                             pk2(win(4 + j - k), win(5 + j - k)));
+                else
+                  sum = pk2(add_(win(4 + j + k), win(4 + j - k)),
+                            add_(win(5 + j + k), win(5 + j - k)));
+                acc = add2(acc, mulp(sum, P.wx[t]));
+              }
+              upk2(add2(pk2(c0, c1), mulp(acc, P.scale)), o.v[j], o.v[j + 1]);
+            }
+          } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const T cc = Cc.v[j];
@@ -161,6 +196,7 @@ __global__ void __launch_bounds__(kResThreads<T>, 1) residentKernel(const ResPar
               acc = add_(acc, mul_(add_(xp, xm), P.wx[t]));
             }
             o.v[j] = add_(cc, mul_(acc, P.scale));
+          }
           }
           T *dst = out + off + h * SP;
           if (x0 + 4 <= P.nx) {
