@@ -6,4 +6,4 @@ for rep in 1 2; do
   HG_LIB=$PWD/paper_2404_02218_b200/lib/variants/libhalogen_b200_r2base.so python tools/sweep.py > gpurun_out/ab/base_$rep.log 2>&1
   python tools/sweep.py > gpurun_out/ab/new_$rep.log 2>&1
 done
-bash tools/gpu_r2_prof.sh
+bash tools/runs/gpu_r2_prof.sh

@@ -11,5 +11,5 @@ for g in 2x1x1 1x1x2; do
 done
 HG_DMP_PROFILE=1 timeout 600 $B --mode strong --grid 1x1x2 --steps 10 --warmup 5 --no-e2e > gpurun_out/r2_bench_e/strong_n2_1x1x2_prof.json 2> gpurun_out/r2_bench_e/strong_n2_1x1x2_prof.err
 timeout 900 python -m pytest tests/test_multigpu.py -m gpu -q -x -p no:cacheprovider -k "x_faces or deep or stuck" > gpurun_out/r2_bench_e/tests_x.log 2>&1
-bash tools/gpu_r2_sanitize.sh
+bash tools/runs/gpu_r2_sanitize.sh
 echo done

@@ -1,4 +1,4 @@
-"""Small cases for compute-sanitizer (tools/gpu_r2_sanitize.sh): every kernel family once,
+"""Small cases for compute-sanitizer (tools/runs/gpu_r2_sanitize.sh): every kernel family once,
 checked against the oracle so a sanitizer run is also a parity run."""
 import os
 import sys
