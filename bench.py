@@ -292,7 +292,8 @@ def workload_config(args, world, transport):
                           if transport == "nccl" else
                           "NVLink P2P stores fused into the stencil kernel (CUDA "
                           "IPC) + system-scope flags; x faces as packed slabs")
-            if world > 1 else "none"}
+            if world > 1 else "none",
+            **({"chunks": args.chunks} if getattr(args, "chunks", 0) else {})}
 
 
 def _slab_module(ref, planes):
@@ -411,6 +412,8 @@ def run_ours(args):
     glob, local, dc, grid, gext = workload_setup(args, world)
     origin = hd.origin_of(rank, grid, list(dc.core[:3])) if dc is not None else None
     plan = hg.Plan(local, local_rank)
+    if args.chunks:
+        plan.set_tuning(chunks=args.chunks)
     plan.init_fields(origin=origin, stream=sh)
     dmp = None
     transport = args.transport
@@ -592,6 +595,8 @@ def main():
     ap.add_argument("--depth", type=int, default=1,
                     help="deep halos at N>1: exchange depth*h-wide halos every `depth` steps")
     ap.add_argument("--workload", default="heat3d_weak", choices=list(WORKLOADS))
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="tuning A/B: z-chunks per column tile (0 = the library's choice)")
     ap.add_argument("--strong-extent", type=int, default=2048)
     ap.add_argument("--e2e-timesteps", type=int, default=100)
     ap.add_argument("--e2e-calls", type=int, default=2)
