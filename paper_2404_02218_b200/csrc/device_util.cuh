@@ -34,8 +34,8 @@ __device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a,
 // (bit-exact: each lane is the scalar RN op).  HG_PACK=2 (product): sums and accumulations as FADD2, every product a scalar
 // FMUL, so ptxas has no mul.f32x2 -> add.f32x2 pair to contract into FFMA2 and no fence is
 // needed; 112 -> ~93 instructions per 4-point plane, +3% burst and +7% sustained (power-capped)
-// on heat 1024^3 (profiles/r2_ab.md).  HG_PACK=1: products packed too, every product fenced
-// (round 1: 4-8% slower, profiles/r1_sweeps.md).  HG_PACK=0: scalar.
+// on heat 1024^3 (profiles/r2_ab.md).  HG_PACK=0: scalar.  (Round 1 also packed the products,
+// each fenced with pfence() below: 4-8% slower, profiles/r1_sweeps.md; that form is gone.)
 #ifndef HG_PACK
 #define HG_PACK 2
 #endif

@@ -93,20 +93,26 @@ int cudaErr(cudaError_t e, const char *what) {
 // would exceed the 227 KB of shared memory at 8 bytes per element).
 template <int RANK, int R, int GEO = 0, int ES = 4> struct StarGeom;
 template <int R, int ES> struct StarGeom<3, R, 1, ES> {
-  static constexpr int TXT = 32, TYT = 12, PTS = 4;
+  static constexpr int TXT = 32, TYT = 12, PTS = 4, YR = 1;
+};
+// GEO 3: a 128 x 16 tile with two output rows per thread (YR): the rows share their y
+// neighbours (10 instead of 14 LDS.128 per 8 points for SDO4), the per-plane bookkeeping is
+// amortised over 8 points, and the taller tile reads 20 rows per 16 instead of 16 per 12
+template <int R, int ES> struct StarGeom<3, R, 3, ES> {
+  static constexpr int TXT = 32, TYT = 8, PTS = 4, YR = 2;
 };
 // GEO 2: the wide tile with 8 x-points per thread (half the threads; per-plane overhead --
 // waits, stage bookkeeping, addressing -- amortised over twice the points)
 template <int R, int ES> struct StarGeom<3, R, 2, ES> {
-  static constexpr int TXT = 16, TYT = 12, PTS = 8;
+  static constexpr int TXT = 16, TYT = 12, PTS = 8, YR = 1;
 };
 template <int R, int ES> struct StarGeom<3, R, 0, ES> {
-  static constexpr int PTS = 4;
+  static constexpr int PTS = 4, YR = 1;
   static constexpr int TXT = R >= 4 ? HG_TXT_R4 : HG_TXT_R2;
   static constexpr int TYT = R >= 4 ? (ES == 8 ? 16 : HG_TYT_R4) : HG_TYT_R2;
 };
 template <int R, int ES> struct StarGeom<2, R, 0, ES> {
-  static constexpr int TXT = 32, TYT = 1, PTS = 4;
+  static constexpr int TXT = 32, TYT = 1, PTS = 4, YR = 1;
 };
 
 #ifndef HG_MINB_G2
@@ -126,9 +132,16 @@ template <int R, int ES> struct StarGeom<2, R, 0, ES> {
 #ifndef HG_L2HINT
 #define HG_L2HINT 1
 #endif
-template <typename T> constexpr bool kPackF32 = HG_PACK == 1 && std::is_same<T, float>::value;
 // HG_PACK=2: x taps at odd offsets (pairs straddling two registers' halves) add scalar
 template <typename T> constexpr bool kPackAdd = HG_PACK == 2 && std::is_same<T, float>::value;
+// does a thread owning YR consecutive rows read row d (relative to its first) as a y neighbour?
+template <int NT, int YR> __device__ constexpr bool yRowNeeded(int d) {
+  for (int yr = 0; yr < YR; ++yr)
+    for (int t = 0; t < NT; ++t)
+      if (d == yr + Taps<NT>::k(t) || d == yr - Taps<NT>::k(t))
+        return true;
+  return false;
+}
 
 template <typename T> struct StarParams {
   int64_t plane;   // elements between consecutive dim-0 planes
@@ -182,7 +195,8 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int TXT = StarGeom<RANK, R, GEO, int(sizeof(T))>::TXT,
                        TYT = StarGeom<RANK, R, GEO, int(sizeof(T))>::TYT;
   static constexpr int PTS = StarGeom<RANK, R, GEO, int(sizeof(T))>::PTS; // x-points/thread
-  static constexpr int TX = TXT * PTS, TY = TYT;
+  static constexpr int YR = StarGeom<RANK, R, GEO, int(sizeof(T))>::YR;   // rows/thread
+  static constexpr int TX = TXT * PTS, TY = TYT * YR;
   static constexpr int PADX = 4;
   static constexpr int CW = TX + 2 * PADX;
   static constexpr int ROWS = TY + 2 * RY;
@@ -191,7 +205,7 @@ template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
   static constexpr int NTHREADS = NCONS + 32;
   // CTAs per SM the register budget must allow (f32 3D: 3 for r<=2, 2 for r=4)
   static constexpr int MINB =
-      GEO == 1 ? 2 : GEO == 2 ? HG_MINB_G2
+      GEO == 1 || GEO == 3 ? 2 : GEO == 2 ? HG_MINB_G2
                    : RANK == 3 ? (sizeof(T) == 4 ? (R <= 2 ? HG_MINB_R2 : HG_MINB_R4) : 1) : 4;
   // f32 3D radius <= 2: the ring is 2Q (heat SDO4) / 3Q (SDO2) slots deep, so the plane loop
   // unrolled over one ring turn has compile-time slot indices (StarCfg::CT; 18% fewer
@@ -379,9 +393,11 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
   const int tx = tid % C::TXT, ty = tid / C::TXT;
   const int lane = tid & 31;
   constexpr int PTS = C::PTS, NV = PTS / 4; // x-points per thread, 4-vectors per row
+  constexpr int YR = C::YR;                 // output rows per thread (tile rows row0 ..)
   const int x0 = tx * PTS;
-  const int rowOwn = (ty + RY) * C::CW;   // own row in a stage
-  T q[Q][PTS];
+  const int row0 = ty * YR;
+  const int rowOwn = (row0 + RY) * C::CW; // own first row in a stage
+  T q[Q][YR][PTS];
 
   auto release = [&](int s) { mbarArrive(&empty[s]); };
 
@@ -393,18 +409,23 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     if (i % ZP == 0)
       mbarWait(&full[s], uint32_t((i / ZP / NS) & 1));
 #pragma unroll
-    for (int h = 0; h < NV; ++h) {
-      V4<T> c = ld4(stages + size_t(s) * C::SSTRIDE + (i % ZP) * C::STAGE + rowOwn + C::PADX +
-                    x0 + 4 * h);
+    for (int yr = 0; yr < YR; ++yr)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        q[i][4 * h + j] = c.v[j];
-    }
+      for (int h = 0; h < NV; ++h) {
+        V4<T> c = ld4(stages + size_t(s) * C::SSTRIDE + (i % ZP) * C::STAGE + rowOwn +
+                      yr * C::CW + C::PADX + x0 + 4 * h);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          q[i][yr][4 * h + j] = c.v[j];
+      }
   }
 
-  const bool yok = RANK == 2 || (yb + ty < P.ny);
+  bool yok[YR];
+#pragma unroll
+  for (int yr = 0; yr < YR; ++yr)
+    yok[yr] = RANK == 2 || (yb + row0 + yr < P.ny);
   T *outRow = P.out + (int64_t(P.zs + zb) * P.plane +
-                       (RANK == 3 ? int64_t(P.ys + yb + ty) * P.pitch : 0) + P.col0 + P.xs +
+                       (RANK == 3 ? int64_t(P.ys + yb + row0) * P.pitch : 0) + P.col0 + P.xs +
                        xb + x0);
   T *dstPlane = outRow; // advanced by one plane per output plane (no per-plane multiply)
   const int xrem = P.nx - (xb + x0);
@@ -446,13 +467,15 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     if (ZP == 1 || zN == 0)
       mbarWait(&full[sN], uint32_t(phN));
 #pragma unroll
-    for (int h = 0; h < NV; ++h) {
-      const V4<T> c = ld4(stages + size_t(sN) * C::SSTRIDE + zN * C::STAGE + rowOwn + C::PADX +
-                          x0 + 4 * h);
+    for (int yr = 0; yr < YR; ++yr)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        q[(U + 2 * R) % Q][4 * h + j] = c.v[j];
-    }
+      for (int h = 0; h < NV; ++h) {
+        const V4<T> c = ld4(stages + size_t(sN) * C::SSTRIDE + zN * C::STAGE + rowOwn +
+                            yr * C::CW + C::PADX + x0 + 4 * h);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          q[(U + 2 * R) % Q][yr][4 * h + j] = c.v[j];
+      }
     if constexpr (!C::CT) {
       if (++zN == ZP) {
         zN = 0;
@@ -464,24 +487,32 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     }
     // x / y neighbours of plane z from its stage
     const T *st = stages + size_t(sC) * C::SSTRIDE + zC * C::STAGE;
-    const V4<T> L = ld4(st + rowOwn + x0);
-    const V4<T> Rr = ld4(st + rowOwn + C::PADX + x0 + PTS);
-    V4<T> yp[NT][NV], ym[NT][NV];
+    V4<T> L[YR], Rr[YR];
+#pragma unroll
+    for (int yr = 0; yr < YR; ++yr) {
+      L[yr] = ld4(st + rowOwn + yr * C::CW + x0);
+      Rr[yr] = ld4(st + rowOwn + yr * C::CW + C::PADX + x0 + PTS);
+    }
+    // rows row0-RY .. row0+YR-1+RY of plane z: the thread's own rows are its queue registers,
+    // the y neighbours outside them staged windows, each loaded once even where two own rows
+    // share it
+    V4<T> yw[YR + 2 * RY][NV];
     if constexpr (RANK == 3) {
 #pragma unroll
-      for (int t = 0; t < NT; ++t)
+      for (int d = -RY; d < YR + RY; ++d)
+        if ((d < 0 || d >= YR) && yRowNeeded<NT, YR>(d))
 #pragma unroll
-        for (int h = 0; h < NV; ++h) {
-          yp[t][h] = ld4(st + rowOwn + Taps<NT>::k(t) * C::CW + C::PADX + x0 + 4 * h);
-          ym[t][h] = ld4(st + rowOwn - Taps<NT>::k(t) * C::CW + C::PADX + x0 + 4 * h);
-        }
+          for (int h = 0; h < NV; ++h)
+            yw[d + RY][h] = ld4(st + rowOwn + d * C::CW + C::PADX + x0 + 4 * h);
     }
-    V4<T> pv[NV];
+    V4<T> pv[YR][NV];
     if constexpr (C::WAVE)
 #pragma unroll
-      for (int h = 0; h < NV; ++h)
-        pv[h] = ld4(pstages + size_t(sC) * C::PSTAGE + zC * (C::TY * C::TX) + ty * C::TX + x0 +
-                    4 * h);
+      for (int yr = 0; yr < YR; ++yr)
+#pragma unroll
+        for (int h = 0; h < NV; ++h)
+          pv[yr][h] = ld4(pstages + size_t(sC) * C::PSTAGE + zC * (C::TY * C::TX) +
+                          (row0 + yr) * C::TX + x0 + 4 * h);
     // the slot is done once its last plane was the computed plane
     const int sDone = (ZP == 1 || zC == ZP - 1) ? sC : -1;
     if constexpr (!C::CT) {
@@ -493,55 +524,17 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     }
 
     constexpr int cz = (U + R) % Q;
-    T o[PTS];
-    if constexpr (kPackF32<T> && PTS == 4) {
-      // points (j, j+1) as one f32x2 lane pair: the same op sequence as the scalar branch
-      // below, every product fenced (see pfence)
-      const uint32_t z0 = P.zero;
-      auto win = [&](int i) -> T { // window [L | centre | Rr]
-        return i < 4 ? L.v[i & 3] : (i < 8 ? q[cz][i & 3] : Rr.v[i & 3]);
-      };
+    // value of point j in row d (relative to row0) of plane z
+    auto yv = [&](int d, int j) -> T {
+      return d >= 0 && d < YR ? q[cz][d][j] : yw[d + RY][j / 4].v[j % 4];
+    };
+    T o[YR][PTS];
 #pragma unroll
-      for (int j = 0; j < 4; j += 2) {
-        const f2 c = pk2(q[cz][j], q[cz][j + 1]);
-        f2 acc = pfence(mul2(c, P.pw0), z0);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int k = Taps<NT>::k(t);
-          const int zp = (U + R + k) % Q, zm = (U + R - k + Q) % Q;
-          acc = add2(acc, pfence(mul2(add2(pk2(q[zp][j], q[zp][j + 1]),
-                                           pk2(q[zm][j], q[zm][j + 1])),
-                                      P.pwz[t]),
-                                 z0));
-        }
-        if constexpr (RANK == 3) {
-#pragma unroll
-          for (int t = 0; t < NT; ++t)
-            acc = add2(acc, pfence(mul2(add2(pk2(yp[t][0].v[j], yp[t][0].v[j + 1]),
-                                             pk2(ym[t][0].v[j], ym[t][0].v[j + 1])),
-                                        P.pwy[t]),
-                                   z0));
-        }
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int k = Taps<NT>::k(t);
-          acc = add2(acc, pfence(mul2(add2(pk2(win(4 + j + k), win(5 + j + k)),
-                                           pk2(win(4 + j - k), win(5 + j - k))),
-                                      P.pwx[t]),
-                                 z0));
-        }
-        f2 r;
-        if constexpr (C::WAVE)
-          r = add2(sub2(pfence(mul2(c, P.ptwo), z0), pk2(pv[0].v[j], pv[0].v[j + 1])),
-                   pfence(mul2(acc, P.pscale), z0));
-        else
-          r = add2(c, pfence(mul2(acc, P.pscale), z0));
-        upk2(r, o[j], o[j + 1]);
-      }
-    } else if constexpr (kPackAdd<T> && PTS == 4) {
+    for (int yr = 0; yr < YR; ++yr) {
+    if constexpr (kPackAdd<T> && PTS == 4) {
       // points (j, j+1): the scalar branch's op sequence, sums and accumulations as f32x2
       auto win = [&](int i) -> T { // window [L | centre | Rr]
-        return i < 4 ? L.v[i & 3] : (i < 8 ? q[cz][i & 3] : Rr.v[i & 3]);
+        return i < 4 ? L[yr].v[i & 3] : (i < 8 ? q[cz][yr][i & 3] : Rr[yr].v[i & 3]);
       };
       auto mulp = [&](f2 v, T w) -> f2 {
         T a, b;
@@ -550,21 +543,24 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
       };
 #pragma unroll
       for (int j = 0; j < 4; j += 2) {
-        const T c0 = q[cz][j], c1 = q[cz][j + 1];
+        const T c0 = q[cz][yr][j], c1 = q[cz][yr][j + 1];
         f2 acc = pk2(mul_(c0, P.w0), mul_(c1, P.w0));
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int k = Taps<NT>::k(t);
           const int zp = (U + R + k) % Q, zm = (U + R - k + Q) % Q;
-          acc = add2(acc, mulp(add2(pk2(q[zp][j], q[zp][j + 1]), pk2(q[zm][j], q[zm][j + 1])),
+          acc = add2(acc, mulp(add2(pk2(q[zp][yr][j], q[zp][yr][j + 1]),
+                                    pk2(q[zm][yr][j], q[zm][yr][j + 1])),
                                P.wz[t]));
         }
         if constexpr (RANK == 3) {
 #pragma unroll
-          for (int t = 0; t < NT; ++t)
-            acc = add2(acc, mulp(add2(pk2(yp[t][0].v[j], yp[t][0].v[j + 1]),
-                                      pk2(ym[t][0].v[j], ym[t][0].v[j + 1])),
+          for (int t = 0; t < NT; ++t) {
+            const int k = Taps<NT>::k(t);
+            acc = add2(acc, mulp(add2(pk2(yv(yr + k, j), yv(yr + k, j + 1)),
+                                      pk2(yv(yr - k, j), yv(yr - k, j + 1))),
                                  P.wy[t]));
+          }
         }
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
@@ -578,58 +574,66 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
         }
         f2 r;
         if constexpr (C::WAVE)
-          r = add2(sub2(pk2(mul_(c0, P.two), mul_(c1, P.two)), pk2(pv[0].v[j], pv[0].v[j + 1])),
+          r = add2(sub2(pk2(mul_(c0, P.two), mul_(c1, P.two)),
+                        pk2(pv[yr][0].v[j], pv[yr][0].v[j + 1])),
                    mulp(acc, P.scale));
         else
           r = add2(pk2(c0, c1), mulp(acc, P.scale));
-        upk2(r, o[j], o[j + 1]);
+        upk2(r, o[yr][j], o[yr][j + 1]);
       }
     } else {
 #pragma unroll
     for (int j = 0; j < PTS; ++j) {
-      const T c = q[cz][j];
+      const T c = q[cz][yr][j];
       // lap = c*W0; then d = 0 (z), 1 (y), rank-1 (x), taps ascending: the generator's
       // op order (kernels.cpp:110-135), one IEEE op at a time
       T acc = mul_(c, P.w0);
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int k = Taps<NT>::k(t);
-        acc = add_(acc, mul_(add_(q[(U + R + k) % Q][j], q[(U + R - k + Q) % Q][j]), P.wz[t]));
+        acc = add_(acc, mul_(add_(q[(U + R + k) % Q][yr][j], q[(U + R - k + Q) % Q][yr][j]),
+                             P.wz[t]));
       }
       if constexpr (RANK == 3) {
 #pragma unroll
-        for (int t = 0; t < NT; ++t)
-          acc = add_(acc, mul_(add_(yp[t][j / 4].v[j % 4], ym[t][j / 4].v[j % 4]), P.wy[t]));
+        for (int t = 0; t < NT; ++t) {
+          const int k = Taps<NT>::k(t);
+          acc = add_(acc, mul_(add_(yv(yr + k, j), yv(yr - k, j)), P.wy[t]));
+        }
       }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int k = Taps<NT>::k(t);
         const int ip = 4 + j + k, im = 4 + j - k; // window [L | centre (PTS) | Rr]
-        const T xp = ip < 4 ? L.v[ip & 3]
-                            : (ip < 4 + PTS ? q[cz][ip - 4] : Rr.v[(ip - 4 - PTS) & 3]);
-        const T xm = im < 4 ? L.v[im & 3]
-                            : (im < 4 + PTS ? q[cz][im - 4] : Rr.v[(im - 4 - PTS) & 3]);
+        const T xp = ip < 4 ? L[yr].v[ip & 3]
+                            : (ip < 4 + PTS ? q[cz][yr][ip - 4] : Rr[yr].v[(ip - 4 - PTS) & 3]);
+        const T xm = im < 4 ? L[yr].v[im & 3]
+                            : (im < 4 + PTS ? q[cz][yr][im - 4] : Rr[yr].v[(im - 4 - PTS) & 3]);
         acc = add_(acc, mul_(add_(xp, xm), P.wx[t]));
       }
       if constexpr (C::WAVE)
-        o[j] = add_(sub_(mul_(c, P.two), pv[j / 4].v[j % 4]), mul_(acc, P.scale));
+        o[yr][j] = add_(sub_(mul_(c, P.two), pv[yr][j / 4].v[j % 4]), mul_(acc, P.scale));
       else
-        o[j] = add_(c, mul_(acc, P.scale));
+        o[yr][j] = add_(c, mul_(acc, P.scale));
     }
     }
-    if (yok) {
-      T *dst = dstPlane;
-      if (xrem >= PTS) {
+    }
 #pragma unroll
-        for (int h = 0; h < NV; ++h)
-          st4(dst + 4 * h, V4<T>{{o[4 * h], o[4 * h + 1], o[4 * h + 2], o[4 * h + 3]}});
-      } else {
+    for (int yr = 0; yr < YR; ++yr)
+      if (yok[yr]) {
+        T *dst = dstPlane + (RANK == 3 ? yr * P.pitch : 0);
+        if (xrem >= PTS) {
 #pragma unroll
-        for (int j = 0; j < PTS; ++j)
-          if (j < xrem)
-            dst[j] = o[j];
+          for (int h = 0; h < NV; ++h)
+            st4(dst + 4 * h,
+                V4<T>{{o[yr][4 * h], o[yr][4 * h + 1], o[yr][4 * h + 2], o[yr][4 * h + 3]}});
+        } else {
+#pragma unroll
+          for (int j = 0; j < PTS; ++j)
+            if (j < xrem)
+              dst[j] = o[yr][j];
+        }
       }
-    }
     dstPlane += P.plane;
     // Release a stage only once the values read from it are consumed.  ptxas may schedule an
     // LDS after the arithmetic that precedes the arrive and complete it after the arrive (the
@@ -657,10 +661,13 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
     // Fused swap of the next step: the send-box points this thread produced (re-read from its
     // own stores, L1/L2-hot) go straight into the neighbours' halos over NVLink.  Done after
     // the plane loop so the streaming loop carries no extra registers.
-    if (yok) {
+#pragma unroll 1
+    for (int yr = 0; yr < YR; ++yr) {
+      if (RANK == 3 && yb + row0 + yr >= P.ny)
+        continue;
       constexpr int XD = RANK - 1;
-      const T *src = outRow;
-      const int64_t e0 = outRow - P.out;
+      const T *src = outRow + (RANK == 3 ? yr * P.pitch : 0);
+      const int64_t e0 = src - P.out;
       for (int d = 0; d < 2 * RANK; ++d) {
         if (!(blockTouch & (1 << d)) || ((P.xpack | P.nodata) & (1 << d)))
           continue;
@@ -674,7 +681,7 @@ __global__ void __launch_bounds__(StarCfg<T, RANK, NT, KIND, GEO>::NTHREADS,
             m0 = max(0, P.nz - P.hs[d] - zb);
           }
         } else if (RANK == 3 && dim == 1) {
-          const int yo = yb + ty;
+          const int yo = yb + row0 + yr;
           if (lo ? yo >= P.hs[d] : yo < P.ny - P.hs[d])
             continue;
         }
@@ -1084,6 +1091,10 @@ template <typename T, int RANK> int dispatchNT(StarLaunch &L, cudaStream_t st, i
       return launchStarT<T, RANK, 1, kHeat, 2>(L, st, b);
     if (L.geo == 2 && s.kind == kHeat && s.ntaps == 2)
       return launchStarT<T, RANK, 2, kHeat, 2>(L, st, b);
+    if (L.geo == 3 && s.kind == kHeat && s.ntaps == 1)
+      return launchStarT<T, RANK, 1, kHeat, 3>(L, st, b);
+    if (L.geo == 3 && s.kind == kHeat && s.ntaps == 2)
+      return launchStarT<T, RANK, 2, kHeat, 3>(L, st, b);
   }
   if (s.kind == kHeat) {
     if (s.ntaps == 1) return launchStarT<T, RANK, 1, kHeat>(L, st, b);
@@ -1578,11 +1589,12 @@ int makeStarTensorMaps(const StarSpec &s, int dtype, int rank, const DevLayout &
   const int es = dtype == HG_F32 ? 4 : 8;
   const int R = s.radius;
   const bool f64 = dtype != HG_F32;
-  // geo 2 is geo 1's 128 x 12 tile with 8 points per thread: same boxes
+  // geo 2 is geo 1's 128 x 12 tile with 8 points per thread: same boxes; geo 3 is 128 x 16
   const int TX = (rank == 3 ? (geo >= 1 ? StarGeom<3, 1, 1>::TXT
                                         : R >= 4 ? StarGeom<3, 4>::TXT : StarGeom<3, 1>::TXT)
                             : StarGeom<2, 1>::TXT) * 4;
-  const int TY = rank == 3 ? (geo >= 1 ? StarGeom<3, 1, 1>::TYT
+  const int TY = rank == 3 ? (geo == 3 ? StarGeom<3, 1, 3>::TYT * StarGeom<3, 1, 3>::YR
+                           : geo >= 1 ? StarGeom<3, 1, 1>::TYT
                                        : R >= 4 ? (f64 ? StarGeom<3, 4, 0, 8>::TYT
                                                        : StarGeom<3, 4>::TYT)
                                                 : StarGeom<3, 1>::TYT)

@@ -318,6 +318,26 @@ def test_two_step_matches_single_step(monkeypatch):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
+# ---- two output rows per thread (GEO 3, 128 x 16 tile) ------------------------------------------
+@pytest.mark.parametrize("order,ext,T", [
+    (4, [24, 16, 128], 3),    # one tile, one chunk
+    (4, [40, 37, 140], 3),    # ragged y (odd: a thread's second row past the domain), ragged x
+    (2, [30, 33, 200], 4),    # SDO2 (radius 1)
+    (4, [300, 50, 260], 2),   # several z-chunks (L2 hints), ragged y and x
+    (4, [36, 800, 1000], 2),  # the benched plane shape class
+])
+def test_two_row_tile_bitwise(port, monkeypatch, order, ext, T):
+    monkeypatch.setenv("HG_STAR_GEO", "3")
+    prog = hg.build_kernel(hg.KernelSpec("heat", 3, 8, order, "f32")).with_extents(ext)
+    arrays = port.initial_fields(prog)
+    perm_o = port.run(prog, arrays, T)
+    _, fin, perm, name = _plan_run(prog, T)
+    assert name.startswith("star3d_r"), name
+    assert perm == perm_o
+    for g, o in zip(fin, [arrays[p] for p in perm_o]):
+        assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
+
+
 # ---- wide-tile geometry of the star kernel (large x-y planes) ---------------------------------
 @pytest.mark.parametrize("order,ext,T", [(4, [36, 800, 1000], 3), (2, [20, 771, 903], 4)])
 def test_wide_tile_geometry_bitwise(port, order, ext, T):
@@ -331,11 +351,12 @@ def test_wide_tile_geometry_bitwise(port, order, ext, T):
         assert np.array_equal(g.view(np.uint32), o.view(np.uint32))
 
 
+@pytest.mark.parametrize("geo", ["1", "3"])
 @pytest.mark.parametrize("spec,grid,T", [(("heat", 3, 24, 4), [2, 2, 1], 4),
                                          (("heat", 3, 32, 2), [1, 2, 2], 3)])
-def test_wide_tile_rank_halos(port, monkeypatch, spec, grid, T):
-    # the wide tile forced on small ranks: per-rank halos after device swaps stay bitwise
-    monkeypatch.setenv("HG_STAR_GEO", "1")
+def test_wide_tile_rank_halos(port, monkeypatch, spec, grid, T, geo):
+    # the wide tiles forced on small ranks: per-rank halos after device swaps stay bitwise
+    monkeypatch.setenv("HG_STAR_GEO", geo)
     prog = hg.build_kernel(hg.KernelSpec(*spec, "f32"))
     local, dc, states = _sim_rank_states(prog, grid, T)
     glob = port.initial_fields(prog)

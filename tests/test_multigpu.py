@@ -76,9 +76,10 @@ def test_nccl_transport_baseline(args):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("geo", ["1", "3"])
 @pytest.mark.parametrize("grid", ["2x1x1", "1x2x2", "2x2x1"])
-def test_ipc_dmp_wide_tile(grid):
-    # the wide star tile (forced) with the fused next-step swap over NVLink
+def test_ipc_dmp_wide_tile(grid, geo):
+    # the wide star tiles (forced) with the fused next-step swap over NVLink
     n = _ngpus()
     nproc = int(np.prod([int(x) for x in grid.split("x")]))
     if n < nproc:
@@ -87,7 +88,7 @@ def test_ipc_dmp_wide_tile(grid):
            str(nproc), os.path.join(REPO, "tools", "dmp_check.py"), "--kind", "heat", "--rank",
            "3", "--extent", "64", "--order", "4", "--T", "6", "--calls", "2,4", "--grid", grid]
     r = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600,
-                       env=dict(os.environ, HG_STAR_GEO="1"))
+                       env=dict(os.environ, HG_STAR_GEO=geo))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
 
