@@ -159,23 +159,27 @@ def test_pw_advection_program():
 
 def test_no_fma_in_stencil_kernels():
     # the bit-exactness contract (no FMA contraction, proj/CMakeLists.txt:8-10) checked on the
-    # shipped SASS: the star kernels carry no FFMA/DFMA/FFMA2 at all; only the generic kernel's
-    # correctly rounded division (__fdiv_rn/__ddiv_rn expansion) may use fused steps
+    # shipped SASS: the star and resident kernels carry no FFMA/DFMA/FFMA2 at all -- their f32
+    # adds run as FADD2 lanes next to scalar FMULs, which ptxas must not fuse; only the generic
+    # kernel's correctly rounded division (__fdiv_rn/__ddiv_rn expansion) may use fused steps
     import shutil
     import subprocess
     if not shutil.which("cuobjdump"):
         pytest.skip("cuobjdump not on PATH")
     sass = subprocess.run(["cuobjdump", "-sass", capi.LIB_PATH], capture_output=True,
                           text=True).stdout
-    fn, bad, seen = None, [], 0
+    fn, bad, seen, packed = None, [], 0, 0
     for line in sass.splitlines():
         if "Function :" in line:
             fn = line.split("Function :")[1].strip()
-            seen += "starKernel" in fn
+            seen += "starKernel" in fn or "residentKernel" in fn
         # (HFMA2 Rx, -RZ, RZ, imm is ptxas' constant-materialisation idiom, not arithmetic)
-        elif fn and "starKernel" in fn and any(op in line for op in ("FFMA", "DFMA")):
-            bad.append((fn, line.strip()))
-    assert seen >= 24
+        elif fn and ("starKernel" in fn or "residentKernel" in fn):
+            if any(op in line for op in ("FFMA", "DFMA")):
+                bad.append((fn, line.strip()))
+            packed += "FADD2" in line
+    assert seen >= 30
+    assert packed > 0  # the f32 instances do run packed adds
     assert not bad, bad[:3]
 
 
