@@ -578,6 +578,8 @@ int jitLaunch(const JitKernel &K, const hg_program &p, const Layout &lay,
   // z-chunks of ~32 planes; ~16 with the 3-deep ring of multi-operand programs (two CTAs per
   // SM: more, shorter units balance the waves)
   const int zc = K.deep <= 3 ? 16 : 32;
+  if (nz <= 0 || ny <= 0 || nx <= 0)
+    return HG_OK; // an empty region: nothing to evaluate
   int nch = chunks > 0 ? chunks : std::max(1, (nz + zc / 2) / zc);
   int chunk = (nz + nch - 1) / nch;
   nch = (nz + chunk - 1) / chunk;
