@@ -24,18 +24,14 @@ __device__ __forceinline__ double sub_(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double div_(double a, double b) { return __ddiv_rn(a, b); }
 
-// ---- packed f32x2 arithmetic (FADD2/FMUL2: two independent IEEE RN f32 ops per issue) -------
-// Each lane of add/mul.rn.f32x2 is the scalar RN op, so packing two points' identical op
-// sequences is bit-exact -- provided nothing is contracted.  ptxas fuses mul.rn.f32x2 ->
-// add.rn.f32x2 into FFMA2 even under -fmad=false (profiles/r1_sweeps.md); pfence() makes a
-// product opaque (OR of a run-time zero into its low word, one ALU op) so every product is
-// rounded before its add, exactly as the reference's -ffp-contract=off code does.
-// f32 stencil arithmetic (star and resident kernels) on f32x2 pairs of neighbouring points
-// (bit-exact: each lane is the scalar RN op).  HG_PACK=2 (product): sums and accumulations as FADD2, every product a scalar
-// FMUL, so ptxas has no mul.f32x2 -> add.f32x2 pair to contract into FFMA2 and no fence is
-// needed; 112 -> ~93 instructions per 4-point plane, +3% burst and +7% sustained (power-capped)
-// on heat 1024^3 (profiles/r2_ab.md).  HG_PACK=0: scalar.  (Round 1 also packed the products,
-// each fenced with pfence() below: 4-8% slower, profiles/r1_sweeps.md; that form is gone.)
+// ---- packed f32x2 arithmetic (FADD2: two independent IEEE RN f32 adds per issue) ---------------
+// f32 stencil arithmetic (star and resident kernels) on f32x2 pairs of neighbouring points:
+// each lane is the scalar RN op, so packing two points' identical op sequences is bit-exact
+// provided nothing is contracted.  HG_PACK=2 (product): sums and accumulations as FADD2, every
+// product a scalar FMUL, so ptxas has no mul.f32x2 -> add.f32x2 pair to fuse into FFMA2 (it
+// does fuse that pair even under -fmad=false; round 1 fenced every packed product instead and
+// ran 4-8% slower, profiles/r1_sweeps.md).  112 -> ~93 instructions per 4-point plane, +3%
+// burst and +7% sustained (power-capped) on heat 1024^3 (profiles/r2_ab.md).  HG_PACK=0: scalar.
 #ifndef HG_PACK
 #define HG_PACK 2
 #endif
@@ -56,19 +52,6 @@ __device__ __forceinline__ f2 add2(f2 a, f2 b) {
 __device__ __forceinline__ f2 sub2(f2 a, f2 b) {
   f2 r;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  f2 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2 pfence(f2 v, uint32_t zero) {
-  uint32_t lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
-  lo |= zero;
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
   return r;
 }
 

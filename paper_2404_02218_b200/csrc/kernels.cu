@@ -183,10 +183,6 @@ template <typename T> struct StarParams {
   unsigned long long put_epoch;
   T *out;
   T w0, wz[3], wy[3], wx[3], scale, two;
-  // f32 packed path: the same weights as {w, w} pairs (uniform registers) and a zero that
-  // only the host knows is zero (pfence)
-  unsigned long long pw0, pwz[3], pwy[3], pwx[3], pscale, ptwo;
-  uint32_t zero;
 };
 
 template <typename T, int RANK, int NT, int KIND, int GEO = 0> struct StarCfg {
@@ -1007,18 +1003,6 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   }
   P.scale = fromBits<T>(s.scale);
   P.two = fromBits<T>(s.two);
-  {
-    auto pair = [](uint64_t b) { return (b & 0xffffffffull) | ((b & 0xffffffffull) << 32); };
-    P.pw0 = pair(s.w0);
-    for (int t = 0; t < 3; ++t) {
-      P.pwz[t] = pair(s.w[0][t]);
-      P.pwy[t] = pair(s.w[RANK == 3 ? 1 : 0][t]);
-      P.pwx[t] = pair(s.w[RANK - 1][t]);
-    }
-    P.pscale = pair(s.scale);
-    P.ptwo = pair(s.two);
-    P.zero = 0;
-  }
   // launch order: the units touching a face that waits for a halo or sends one go last, so
   // their waits (and the peers' flags, published at the end of the peers' previous step)
   // overlap the interior units
