@@ -586,7 +586,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--extent", type=int, default=1024)
     ap.add_argument("--grid", default=None, help="process grid AxBxC (default: weak N x 1 x 1, "
-                                                 "strong 1/2x1x1/2x2x1/2x2x2)")
+                                                 "strong 1/2x1x1/2x2x1/2x4x1)")
     ap.add_argument("--mode", default="weak", choices=["weak", "strong"])
     ap.add_argument("--transport", default="auto", choices=["auto", "p2p", "nccl"],
                     help="halo transport at N>1: p2p = fused NVLink stores from the stencil "

@@ -28,9 +28,11 @@ def weak_grid(world: int, ndim: int = 3) -> List[int]:
 
 
 def strong_grid(world: int) -> List[int]:
-    """Near-cubic process grids for a fixed global domain (1, 2x1x1, 2x2x1, 2x2x2); the x
-    faces of 2x2x2 travel as packed slabs on the fused path."""
-    table = {1: [1, 1, 1], 2: [2, 1, 1], 4: [2, 2, 1], 8: [2, 2, 2]}
+    """Process grids (z, y, x) for a fixed global domain that keep x, the contiguous dim,
+    whole: 1, 2x1x1, 2x2x1, 2x4x1.  Grids splitting x work (packed slabs on the fused path)
+    but ran 11% slower at N=4 (1x2x2 2439 vs 2x2x1 2739 GPts/s); rank shapes with x = 2048 and
+    y = 512 ran fastest alone (profiles/r2_geo_ab.log)."""
+    table = {1: [1, 1, 1], 2: [2, 1, 1], 4: [2, 2, 1], 8: [2, 4, 1]}
     if world in table:
         return table[world]
     return weak_grid(world)

@@ -76,5 +76,5 @@ def test_handle_exchange(world, grid):
 def test_grids():
     from paper_2404_02218_b200 import dist as hd
     assert hd.weak_grid(8) == [8, 1, 1]
-    assert hd.strong_grid(8) == [2, 2, 2] and hd.strong_grid(4) == [2, 2, 1]
+    assert hd.strong_grid(8) == [2, 4, 1] and hd.strong_grid(4) == [2, 2, 1]
     assert hd.face_neighbors(0, [2, 2, 2]) == [4, 2, 1]
