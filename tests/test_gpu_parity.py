@@ -240,6 +240,7 @@ def _sim_rank_states(prog, grid, T):
     (("heat", 3, 16, 4), [2, 2, 2], 3), (("wave", 3, 24, 8), [3, 1, 2], 4),
     (("heat", 2, 30, 2), [3, 2], 5), (("wave", 2, 40, 4), [2, 4], 3),
     (("heat", 3, 32, 2), [4, 1, 1], 2),
+    (("heat", 3, 32, 4), [2, 4, 1], 3),  # the N=8 strong grid (strong_grid(8))
 ])
 def test_rank_halos_bitwise_after_swaps(port, spec, grid, T):
     # per-rank local state (cores AND halos) == the oracle's restatement of RankHooks::swap
