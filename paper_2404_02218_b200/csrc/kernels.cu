@@ -896,11 +896,45 @@ int launchStarT(StarLaunch &L, cudaStream_t st, int *blocks_out) {
   P.tiles_y = (P.ny + C::TY - 1) / C::TY;
   const int ntiles = P.tiles_x * P.tiles_y;
   int chunks = L.chunks;
+  // CTAs resident at once (per device; the occupancy query runs once per kernel and device)
+  auto residentSlots = [&]() -> long {
+    static std::mutex omu;
+    static int slots[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(omu);
+    int &sl = slots[dev & 63];
+    if (sl == 0) {
+      int sms = 148, per = 1;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::NTHREADS, C::SMEM);
+      sl = sms * std::max(per, 1);
+    }
+    return sl;
+  };
   if (chunks <= 0 && RANK == 3) {
     // ~32R planes per chunk: short-lived CTAs keep neighbouring tiles in step (their shared
     // halo rows then hit in L2), while the 2R-plane chunk overlap stays ~6% (measured sweep,
     // profiles/README.md)
     chunks = std::max(1, (P.nz + 16 * C::R) / (32 * C::R));
+    // a launch of few waves: its partly empty last wave is a visible share of the step, so
+    // take the chunk count up to 1.5x that fills it best (heat 512^3: 8 -> 12 chunks, 4.65 ->
+    // 6.97 waves, 636-659 -> 669-673 GPts/s sustained; profiles/r2_ab.md).  Many waves keep
+    // the default (1024^3: 37 waves).  Plain single-GPU steps only: the dmp launches keep the
+    // chunking their multi-GPU tests ran with.
+    const long slots = residentSlots();
+    auto fill = [&](int c) {
+      const int len = (P.nz + c - 1) / c;
+      const long units = long(ntiles) * ((P.nz + len - 1) / len);
+      return double(units) / double((units + slots - 1) / slots * slots);
+    };
+    if (!L.fuse && !L.wait_flags && long(ntiles) * chunks < 10 * slots) {
+      int best = chunks;
+      for (int c = chunks + 1; c <= std::min(P.nz, chunks + chunks / 2); ++c)
+        if (fill(c) > fill(best) + 1e-9)
+          best = c;
+      chunks = best;
+    }
   }
   if (chunks <= 0) {
     // pick the z-chunk count minimising waves x (planes + pipeline fill) per CTA
