@@ -614,7 +614,10 @@ extern "C" int hg_apply_compile(const hg_program *prog, char *src, size_t cap,
   std::string why;
   if (!jitEligible(*prog, a, &why))
     return setError(HG_EUNSUPPORTED, "fused apply family: " + why);
-  JitKernel K;
+  JitKernel K; // the codegen a plan created now would use (its knobs: HG_JIT_PACK, HG_JIT_DEPTH)
+  const Knobs kn = readKnobs();
+  K.pack = kn.jitPack;
+  K.deep = kn.jitDepth;
   st = jitBuildSource(*prog, K);
   if (st)
     return st;

@@ -145,8 +145,27 @@ def test_fused_apply_family_generates_and_compiles(golden):
         assert rc == 0, capi.lib().hg_last_error()
         assert n.value > 1000 and b"hg_apply" in buf.value
         assert b"__fadd_rn" in buf.value or b"__dadd_rn" in buf.value
+        # one persistent wave walks the units, the TMA ring running across them
+        assert b"u < P.units; u += gridDim.x" in buf.value
         done += 1
     assert done >= 4
+
+
+@pytest.mark.parametrize("pack", ["0", "1"])
+def test_fused_apply_pw_codegen(monkeypatch, pack):
+    # the PW set (config 4) through both codegens: scalar, and f32 adds as FADD2 lanes with
+    # scalar products (HG_JIT_PACK=1); both compile for sm_100a
+    import ctypes as C
+    monkeypatch.setenv("HG_JIT_PACK", pack)
+    p = hg.Program.pw_advection(32, 64, 64)
+    buf = C.create_string_buffer(1 << 21)
+    n = C.c_size_t()
+    assert capi.lib().hg_apply_compile(C.byref(p.prog), buf, 1 << 21, C.byref(n)) == 0, \
+        capi.lib().hg_last_error()
+    src = buf.value
+    assert n.value > 1000
+    assert (b"upk2(add2(pk2(" in src) == (pack == "1")
+    assert b"mul.rn.f32x2" not in src  # products are never packed (no FFMA2 contraction)
 
 
 def test_pw_advection_program():
